@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: SIDWT lifting + correlation throughput (complex samples/s) on B200.
+
+One step = one pass of the whole hot path over one batch:
+sidwt_analyze (fused J-level lifting, all shift branches) + sidwt_correlate_peaks
+(correlation at every scale and lag, written to HBM, plus the per-scale peak
+search), on inputs already resident in HBM.  Workload: BASELINE.json configs[1]
+(C2, causal Daubechies-4, J=5, symmetric, 4096 x 4096 complex64, Barker-13x10),
+override with --config.  Multi-GPU (torchrun): weak scaling, each rank its own
+batch of rows, no collective on the data path.
+
+--impl reference times the CPU oracle (oracle/, fp64 C, OpenMP) on the host
+cores, each step a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "complex samples/s through SIDWT lifting+correlation"
+UNIT = "complex samples/s"
+FP32_LANES_PER_SM = 128
+N_SMS = 148
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm=float(d["hbm_gbs"]), sm_mhz=float(d.get("sm_max_mhz", 1965.0)), src="measured")
+    except Exception:
+        return dict(hbm=6650.0, sm_mhz=1965.0, src="fallback")
+
+
+def fp32_peak_tflops(sm_mhz):
+    # derived from the unit counts: 148 SMs x 128 FP32 lanes x 2 flop/FFMA x clock
+    return N_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic(cfg, plan):
+    """Per-row algorithmic bytes / flops of each kernel."""
+    J, N = cfg.levels, cfg.N
+    sb = 4 if cfg.is_int else 8
+    stride = plan.band_stride
+    k1_bytes = N * sb + (J + 1) * 2 * stride * 4
+    taps = sum(c for c in plan_counts(plan))
+    k2_flops = cfg.n_templates * N * taps * 8            # 4 FFMA per complex MAC (8 flop)
+    k2_bytes = (J + 1) * 2 * stride * 4 + cfg.n_templates * (J + 1) * N * 8
+    return dict(k1_bytes=k1_bytes, k2_flops=k2_flops, k2_bytes=k2_bytes, taps=taps)
+
+
+def plan_counts(plan):
+    from paper_cs_0607001_b200 import _native
+    J = plan.levels
+    kmin = np.zeros(J + 1, np.int32)
+    cnt = np.zeros(J + 1, np.int32)
+    _native.sidwt_template_taps(plan.handle, None, kmin, cnt)
+    return [int(c) for c in cnt]
+
+
+def traffic_from_profiles(cfg_name, kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(cfg_name, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, tm, budget_s=15.0):
+    """The oracle as it stands, on the host cores, on a bounded row sample."""
+    import oracle as O
+    threads = O.max_threads()
+    probe = W.make_rows(cfg, 0, min(cfg.rows, threads), tm)
+    t0 = time.perf_counter()
+    O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, probe, tm, corr=True, nthreads=threads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    per_row = dt / probe.shape[0]
+    n = int(max(probe.shape[0], min(cfg.rows, budget_s / per_row)))
+    rows = W.make_rows(cfg, 0, n, tm)
+    t0 = time.perf_counter()
+    O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, rows, tm, corr=True, nthreads=threads)
+    dt = time.perf_counter() - t0
+    cpu = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"value": n * cfg.N / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{n} of {cfg.rows} rows of {cfg.name} (full N={cfg.N}, all {cfg.levels + 1} scales, "
+                      f"{cfg.n_templates} template(s)), fp64 C oracle, {dt:.1f} s, cpu '{cpu}'"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle on this workload (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle as O
+    tm = W.templates(cfg)
+    threads = O.max_threads()
+    probe = W.make_rows(cfg, 0, min(cfg.rows, threads), tm)
+    t0 = time.perf_counter()
+    O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, probe, tm, nthreads=threads)
+    per_row = max((time.perf_counter() - t0) / probe.shape[0], 1e-6)
+    total_budget = 120.0
+    n = int(max(1, min(cfg.rows, total_budget / (args.steps + args.warmup) / per_row)))
+    rows = W.make_rows(cfg, 0, n, tm)
+    for _ in range(args.warmup):
+        O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, rows, tm, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, rows, tm, nthreads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = n * cfg.N / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "i64" if cfg.is_int else "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{cfg.name}: {cfg.description}", "rows_per_step": n, "N": cfg.N},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{n} rows of {cfg.name} per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--rows", type=int, default=0, help="override batch rows (default: the config's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = W.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_cs_0607001_b200 import Plan, _native
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    R = args.rows or cfg.rows
+    tm = W.templates(cfg)
+    rows_h = W.make_rows(cfg, rank * R, R, tm)          # weak scaling: each rank its own batch
+    plan = Plan(cfg.family, cfg.levels, cfg.N, R, cfg.ext, device=dev).load_templates(tm)
+    stream = torch.cuda.current_stream(dev)
+    d_rows = plan.rows_to_device(rows_h)
+    bands = plan.empty_bands(R)
+    corr = plan.empty_corr(R)
+    lag, val = plan.empty_peaks(R)
+
+    def step():
+        plan.analyze(d_rows, R, bands, stream)
+        plan.correlate_peaks(bands, R, corr, lag, val, stream=stream)
+
+    launches_per_step = 1 + 2
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # per-kernel timing (CUDA events on the launching stream), separate pass
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    k1_ms, k2_ms = [], []
+    for _ in range(max(3, min(args.steps, 10))):
+        ev[0].record(stream)
+        plan.analyze(d_rows, R, bands, stream)
+        ev[1].record(stream)
+        plan.correlate_peaks(bands, R, corr, lag, val, stream=stream)
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        k1_ms.append(ev[0].elapsed_time(ev[1]))
+        k2_ms.append(ev[1].elapsed_time(ev[2]))
+    k1_ms = float(np.median(k1_ms))
+    k2_ms = float(np.median(k2_ms))
+
+    # timed region: K steps, barrier + sync on both sides, max over ranks
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * R * cfg.N / (ms * 1e-3)
+
+    # e2e: host rows (pinned) -> device -> path -> lag/val back to host, through the C ABI
+    e2e = None
+    if not args.no_e2e:
+        sb = 4 if cfg.is_int else 8
+        h_rows = torch.from_numpy(np.ascontiguousarray(rows_h).view(np.uint8).reshape(-1)).pin_memory()
+        h_lag = torch.empty(lag.shape, dtype=torch.int32).pin_memory()
+        h_val = torch.empty(val.shape, dtype=val.dtype).pin_memory()
+        plan.execute_host(h_rows, R, h_lag, h_val, stream)
+        torch.cuda.synchronize()
+        for _ in range(2):
+            plan.execute_host(h_rows, R, h_lag, h_val, stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.execute_host(h_rows, R, h_lag, h_val, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        assert np.array_equal(h_lag.numpy(), lag.cpu().numpy()), "e2e lags differ from the device path"
+        e2e = {"value": world * R * cfg.N / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": R * cfg.N * sb,
+               "d2h_bytes_per_step": int(h_lag.numel() * 4 + h_val.numel() * 4),
+               "ms_per_step": ems}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    pk = load_peaks()
+    alg = algorithmic(cfg, plan)
+    k1_gbs = R * alg["k1_bytes"] / (k1_ms * 1e-3) / 1e9
+    k2_tflops = R * alg["k2_flops"] / (k2_ms * 1e-3) / 1e12
+    k2_gbs = R * alg["k2_bytes"] / (k2_ms * 1e-3) / 1e9
+    fp32_peak = fp32_peak_tflops(pk["sm_mhz"])
+    stages = {
+        "analyze": {"kernel": "k_analyze", "ms": k1_ms, "bound": "hbm", "achieved": k1_gbs, "peak": pk["hbm"],
+                    "unit": "GB/s", "frac": k1_gbs / pk["hbm"], "bytes_per_row": alg["k1_bytes"]},
+        "correlate_peaks": {"kernel": "k_correlate+k_peaks_finalize", "ms": k2_ms,
+                            "alu": {"achieved": k2_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+                                    "frac": k2_tflops / fp32_peak, "flops_per_row": alg["k2_flops"]},
+                            "hbm": {"achieved": k2_gbs, "peak": pk["hbm"], "unit": "GB/s",
+                                    "frac": k2_gbs / pk["hbm"], "bytes_per_row": alg["k2_bytes"]}},
+    }
+    if k2_ms >= k1_ms:
+        a2, h2 = stages["correlate_peaks"]["alu"], stages["correlate_peaks"]["hbm"]
+        use = a2 if a2["frac"] >= h2["frac"] else h2
+        roof = {"kernel": "k_correlate", "bound": "alu" if use is a2 else "hbm", "achieved": use["achieved"],
+                "peak": use["peak"], "unit": use["unit"], "frac": use["frac"],
+                "traffic": traffic_from_profiles(cfg.name, "k_correlate"),
+                "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x %.0f MHz" % pk["sm_mhz"])
+                if use is a2 else f"{pk['src']} MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        a1 = stages["analyze"]
+        roof = {"kernel": "k_analyze", "bound": "hbm", "achieved": a1["achieved"], "peak": a1["peak"],
+                "unit": "GB/s", "frac": a1["frac"], "traffic": traffic_from_profiles(cfg.name, "k_analyze"),
+                "peak_source": f"{pk['src']} MEASURED_PEAKS.json hbm_gbs"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "i32" if cfg.is_int else "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "rows_per_gpu": R, "N": cfg.N,
+                   "levels": cfg.levels, "templates": cfg.n_templates, "parallelism": f"rows x{world} (weak)",
+                   "l2": "no flush: per-step working set (bands %.2f GB + corr %.2f GB) >> 126 MB L2" % (
+                       R * (cfg.levels + 1) * 2 * plan.band_stride * 4 / 1e9,
+                       R * cfg.n_templates * (cfg.levels + 1) * cfg.N * 8 / 1e9)},
+        "roofline": roof,
+        "stages": stages,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, tm)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

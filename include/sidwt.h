@@ -1,0 +1,168 @@
+/*
+ * sidwt.h -- C ABI of libsidwt: SIDWT-domain multiresolution correlation of
+ * complex radar range lines by lifting, B200 (sm_100a) implementation of the
+ * hot path of C. Bhattacharya & P.R. Mahapatra, "A Novel Application of
+ * Lifting Scheme for Multiresolution Correlation of Complex Radar Signals"
+ * (arXiv cs/0607001).  Citations "PAPER.md:L" are lines of the paper text.
+ *
+ * What is computed (DESIGN.md section 1 gives every reading in full):
+ *   Each received row y (N complex samples) is extended once (periodic, or
+ *   whole-sample symmetric about 0 and N-1) and decomposed by the dual-analysis
+ *   lifting program of the chosen family at EVERY fine-grid position and every
+ *   level s = 1..J.  This is the paper's even/odd-shift SIDWT tree (PAPER.md:
+ *   65-73, 276-282, Fig. 1/5) with branch r, coefficient k stored at
+ *   tau = r + 2^s k.  It yields detail bands W_1..W_J and the approximation
+ *   band U_J.  The template x (T samples, zero outside [0,T)) is decomposed
+ *   critically sampled by the analysis lifting program ("stored"):
+ *   b_1..b_J, a_J.  The correlation at scale s = 0..J and lag tau in [0,N) is
+ *   the eq. (4) sum over the levels coarser than s:
+ *       corr_J[tau] = sum_k conj(a_J[k]) U_J[tau + 2^J k]
+ *       corr_s[tau] = corr_{s+1}[tau] + sum_k conj(b_{s+1}[k]) W_{s+1}[tau + 2^{s+1} k]
+ *   corr_0 equals the textbook correlation sum_n conj(x[n]) ybar[n + tau];
+ *   corr_s = < (scale-s approximation of x), (scale-s dual approximation of
+ *   the row shifted by tau) > (eq. (5),(15),(20),(20a), PAPER.md:75-85,141-145,
+ *   284-290).  Complex signals are the linear sum of real SIDWTs of Re and Im
+ *   (PAPER.md:296, 322); the analytic factor 2 of eq. (19) is omitted.
+ *
+ * Families (lifting programs, section III):
+ *   SIDWT_LEGALL53      LeGall 5/3, PAPER.md:187-213 (dual program PAPER.md:211)
+ *   SIDWT_CDF97         CDF 9/7 with Table I's rational parameters,
+ *                       PAPER.md:215-244 (reading R-D3 of the garbled grids)
+ *   SIDWT_DAUB4_CAUSAL  causal Daubechies-4, eq. (17)
+ *                       (readings R-D1: pairs (x[2k], x[2k-1]); R-D2)
+ *   SIDWT_LEGALL53_INT  reversible integer 5/3 (floor-rounded predict/update,
+ *                       PAPER.md:13, 326, refs [9],[25]; reading R-INT), int16
+ *                       I/Q rows, int32 coefficients, int32 wrap-around sums
+ *
+ * Conventions common to all calls
+ *   - Device pointers are caller-owned (e.g. torch tensors' data_ptr()), 16-byte
+ *     aligned.  Host pointers are caller-owned.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every device
+ *     call is stream-ordered and non-blocking; no call synchronises the host.
+ *     Launch failures return SIDWT_ERR_CUDA; faults inside kernels surface at
+ *     the caller's next synchronisation.  No C++ exception crosses the ABI.
+ *   - A plan is used by one stream at a time; it holds no global state.
+ *   - Arguments are validated before any device work; on error nothing is
+ *     launched and outputs are untouched.
+ */
+#ifndef SIDWT_H
+#define SIDWT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sidwt_plan_s* sidwt_plan;
+
+typedef enum {
+    SIDWT_OK = 0,
+    SIDWT_ERR_PARAM = 1,      /* bad enum, null pointer, N not a power of two >= 2   */
+    SIDWT_ERR_LENGTH = 2,     /* template length T not in [1, N]       */
+    SIDWT_ERR_DIMENSION = 3,  /* rows not in [1, batch], n_templates < 1             */
+    SIDWT_ERR_DEPTH = 4,      /* levels < 1 or 2^levels > N, or levels > 16 */
+    SIDWT_ERR_RANGE = 5,      /* size product overflows / exceeds device limits      */
+    SIDWT_ERR_STATE = 6,      /* analyze/correlate before template_load              */
+    SIDWT_ERR_OOM = 7,        /* device allocation failed                            */
+    SIDWT_ERR_CUDA = 8        /* CUDA runtime error (launch failure, no device, ...)  */
+} sidwt_status;
+
+typedef enum {
+    SIDWT_LEGALL53 = 0,
+    SIDWT_CDF97 = 1,
+    SIDWT_DAUB4_CAUSAL = 2,
+    SIDWT_LEGALL53_INT = 3
+} sidwt_filter;
+
+typedef enum {
+    SIDWT_EXT_PERIODIC = 0,   /* ybar(n) = y[n mod N]                                   */
+    SIDWT_EXT_SYMMETRIC = 1   /* whole-sample symmetric about 0 and N-1 (period 2N-2)   */
+} sidwt_ext;
+
+#define SIDWT_MAX_LEVELS 16
+
+/* Create a plan.  filter: sidwt_filter; levels J >= 1 with 2^J <= N; N a power
+ * of two >= 2; batch >= 1 is the largest `rows` any later call will pass;
+ * ext: sidwt_ext.  Validation only (no device memory is touched), so it also
+ * works on a machine without a GPU.  *out receives the plan. */
+sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t N,
+                               int64_t batch, int ext);
+
+/* Free the plan and every device buffer it owns.  NULL is accepted. */
+sidwt_status sidwt_plan_destroy(sidwt_plan plan);
+
+/* Load the template bank and build its analysis pyramid on the device.
+ * host_templates: host memory, [n_templates][T] complex64 (float2: re, im) for
+ * the float families, int16x2 (I, Q) for SIDWT_LEGALL53_INT.  1 <= T <= N.
+ * The pyramid is computed by a device kernel in double (int64 for the integer
+ * family) and stored as float2 / int2 taps; this call synchronises the device
+ * once (template loading is not on the per-pulse path).  Fixes
+ * sidwt_band_stride / sidwt_band_offset.  May be called again (reload). */
+sidwt_status sidwt_template_load(sidwt_plan plan, const void* host_templates, int64_t T,
+                                 int n_templates);
+
+/* Decompose rows by lifting (every level, both shift branches).
+ * d_rows : device, [rows][N] complex64, or int16x2 for the integer family.
+ * d_bands: device, [rows][levels+1][2][band_stride] float32 (int32 for the
+ *          integer family), split-complex: plane 0 = Re, plane 1 = Im.  Band
+ *          b < levels holds W_{b+1}, band `levels` holds U_J.  Fine-grid position
+ *          p is stored at index p + band_offset, for p in
+ *          [-band_offset, band_stride - band_offset); the whole plane is written.
+ * Requires template_load (the band margins depend on the template support). */
+sidwt_status sidwt_analyze(sidwt_plan plan, const void* d_rows, int64_t rows, void* d_bands,
+                           void* stream);
+
+/* Correlate bands against every loaded template at every scale and lag.
+ * d_corr: device, [rows][n_templates][levels+1][N] complex64 (int32x2 for the
+ *         integer family: the exact integer correlation reduced mod 2^32).
+ *         Scale index s = 0 (finest, = textbook correlation) .. levels (U_J only). */
+sidwt_status sidwt_correlate(sidwt_plan plan, const void* d_bands, int64_t rows, void* d_corr,
+                             void* stream);
+
+/* Peak search ("sample index l for maximum matching"): for every
+ * (row, template, scale) the smallest lag tau in [0,N) maximising |corr|^2
+ * (fp32 |.|^2 for float families; exact uint64 for the integer family).
+ * d_lag: device [rows][n_templates][levels+1] int32; d_val: same shape,
+ * complex64 (int32x2) value at that lag; d_val may be NULL. */
+sidwt_status sidwt_peaks(sidwt_plan plan, const void* d_corr, int64_t rows, int32_t* d_lag,
+                         void* d_val, void* stream);
+
+/* Fused correlate + peaks (same outputs as sidwt_correlate followed by
+ * sidwt_peaks; the peak search is folded into the correlation epilogue so
+ * the correlation is not read back from HBM).  d_corr may be NULL ("peaks
+ * only": nothing but lag/val is written). */
+sidwt_status sidwt_correlate_peaks(sidwt_plan plan, const void* d_bands, int64_t rows,
+                                   void* d_corr, int32_t* d_lag, void* d_val, void* stream);
+
+/* End-to-end from HOST memory: copy rows host->device, analyze, correlate,
+ * peaks, copy lag (and val if non-NULL) device->host, all on `stream`.
+ * Uses plan-owned device buffers (allocated on first use for `batch` rows;
+ * SIDWT_ERR_OOM if they do not fit).  h_rows should be pinned for overlap.
+ * Returns after enqueueing; synchronise `stream` before reading h_lag/h_val. */
+sidwt_status sidwt_execute_host(sidwt_plan plan, const void* h_rows, int64_t rows,
+                                int32_t* h_lag, void* h_val, void* stream);
+
+/* Layout queries (valid after template_load; -1 before). */
+int64_t sidwt_band_stride(sidwt_plan plan);   /* >= band_offset + N + right margin, multiple of 32 */
+int64_t sidwt_band_offset(sidwt_plan plan);   /* 0 (periodic) or the left margin M_L (symmetric)    */
+int64_t sidwt_bands_bytes(sidwt_plan plan, int64_t rows);
+int64_t sidwt_corr_bytes(sidwt_plan plan, int64_t rows);
+
+/* Copy the device template pyramid to host: for each template, terms
+ * b_1..b_J then a_J, each `count` taps starting at coefficient index kmin
+ * (kmin/count per term written to kmin[J+1], count[J+1] when non-NULL);
+ * taps as float2 (int2 for the integer family), unconjugated.  host_taps may
+ * be NULL to query only.  Returns the number of taps per template or -1. */
+int64_t sidwt_template_taps(sidwt_plan plan, void* host_taps, int32_t* kmin, int32_t* count);
+
+/* Number of kernel launches the last analyze / correlate / peaks / correlate_peaks
+ * call enqueued (for launch accounting). */
+int sidwt_last_launches(sidwt_plan plan);
+
+const char* sidwt_status_string(sidwt_status st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIDWT_H */

@@ -1,0 +1,527 @@
+// kernels.cuh -- sm_100a kernels of libsidwt.
+//   k_template_pyramid : analysis pyramid of the template bank (fp64 / int64)
+//   k_analyze          : fused J-level dual-analysis lifting of one (row, component,
+//                        tile), all levels on chip, bands stored by TMA bulk copies
+//   k_correlate        : per-scale correlation (eq. (4) suffix sums), register-blocked
+//                        sliding window, fused per-tile peak partials
+//   k_peaks / k_peaks_finalize : argmax over lags (smallest lag on ties)
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <type_traits>
+
+#include "lifting.cuh"
+
+namespace sidwt {
+
+constexpr int kMaxTerms = 17;   // J + 1 <= SIDWT_MAX_LEVELS + 1
+
+// ---------------------------------------------------------------------------
+// PTX helpers: bulk async copy smem -> global (TMA engine, SASS UBLKCP).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+               :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Extension of the received row (DESIGN.md R-D6): periodic or whole-sample symmetric.
+__device__ __forceinline__ int ext_index(long long n, int N, int ext) {
+  if (ext == 0) {
+    long long m = n % N;
+    return (int)(m < 0 ? m + N : m);
+  }
+  if (N == 1) return 0;
+  const long long P = 2LL * N - 2;
+  long long m = n % P;
+  if (m < 0) m += P;
+  return (int)(m < N ? m : P - m);
+}
+
+// ---------------------------------------------------------------------------
+// K0: template pyramid.  One thread per (template, component); analysis lifting
+// programs on the zero-extended template, critically sampled, in fp64 (int64).
+// ---------------------------------------------------------------------------
+struct PyrParams {
+  int fam, J, T, n_t, taps_per_t;
+  int klo[kMaxTerms], cnt[kMaxTerms], off[kMaxTerms];   // term i: b_{i+1} (i<J), a_J (i=J)
+  int scratch_len;                                      // per-thread scratch length (doubles)
+};
+
+template <typename V>
+__device__ __forceinline__ V getz(const V* a, long lo, long hi, long n) {
+  return (n < lo || n > hi) ? V(0) : a[n - lo];
+}
+
+template <typename V>
+__device__ void analysis_level(int fam, const V* cur, long lo, long hi, V* e, V* o, long klo, long khi) {
+  // fill e/o over [klo, khi]; conv A: (x[2k], x[2k+1]); causal D4 (R-D1): (x[2k], x[2k-1])
+  for (long k = klo; k <= khi; ++k) {
+    e[k - klo] = getz(cur, lo, hi, 2 * k);
+    o[k - klo] = getz(cur, lo, hi, fam == FD4 ? 2 * k - 1 : 2 * k + 1);
+  }
+  const long n = khi - klo + 1;
+  auto E = [&](long i) -> V { return (i < 0 || i >= n) ? V(0) : e[i]; };
+  auto O = [&](long i) -> V { return (i < 0 || i >= n) ? V(0) : o[i]; };
+  if (fam == F53) {
+    for (long i = 0; i < n; ++i) o[i] = o[i] - V(0.5) * (E(i) + E(i + 1));
+    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(0.25) * (O(i) + O(i - 1));
+    for (long i = 0; i < n; ++i) o[i] = V(0.5) * o[i];
+  } else if (fam == F97) {      // PAPER.md:238, reading R-D3
+    for (long i = 0; i < n; ++i) o[i] = o[i] + V(kAlpha) * (E(i) + E(i + 1));
+    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(kBeta) * (O(i) + O(i - 1));
+    for (long i = 0; i < n; ++i) o[i] = o[i] + V(kGamma) * (E(i) + E(i + 1));
+    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(kDelta) * (O(i) + O(i - 1));
+    for (long i = 0; i < n; ++i) { e[i] = V(kZeta) * e[i]; o[i] = o[i] / V(kZeta); }
+  } else if (fam == FD4) {      // eq. (17)
+    for (long i = 0; i < n; ++i) o[i] = o[i] - V(kSqrt3) * e[i];
+    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(kD4c1) * O(i) + V(kD4c2) * O(i - 1);
+    for (long i = n - 1; i >= 0; --i) o[i] = E(i) + O(i - 1);
+    for (long i = 0; i < n; ++i) { e[i] = V(kD4K1) * e[i]; o[i] = V(kD4K2) * o[i]; }
+  }
+}
+
+__device__ void analysis_level_int(const int64_t* cur, long lo, long hi, int64_t* e, int64_t* o, long klo, long khi) {
+  for (long k = klo; k <= khi; ++k) {
+    e[k - klo] = getz(cur, lo, hi, 2 * k);
+    o[k - klo] = getz(cur, lo, hi, 2 * k + 1);
+  }
+  const long n = khi - klo + 1;
+  // o -= (e_k + e_{k+1}) >> 1 ; e += (o_{k-1} + o_k + 2) >> 2   (reading R-INT)
+  for (long i = 0; i < n; ++i) o[i] -= (e[i] + (i + 1 < n ? e[i + 1] : 0)) >> 1;
+  for (long i = n - 1; i >= 0; --i) e[i] += ((i > 0 ? o[i - 1] : 0) + o[i] + 2) >> 2;
+}
+
+__host__ __device__ inline long fl_div2(long a) { return a >= 0 ? a / 2 : -((-a + 1) / 2); }
+__host__ __device__ inline long cl_div2(long a) { return -fl_div2(-a); }
+
+// table: [n_t][taps_per_t] float2 (or int2); scratch: per thread 4 * scratch_len values
+__global__ void k_template_pyramid(const void* __restrict__ x, void* __restrict__ table,
+                                   double* __restrict__ scratch, PyrParams p) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= 2 * p.n_t) return;
+  const int t = gid >> 1, comp = gid & 1;
+  const Supp sp = analysis_support(p.fam);
+  const bool isint = (p.fam == FI53);
+  double* base = scratch + (size_t)gid * 4 * p.scratch_len;
+  long lo = 0, hi = p.T - 1;
+  if (!isint) {
+    double* cur = base;
+    double* nxt = base + p.scratch_len;
+    double* e = base + 2 * p.scratch_len;
+    double* o = base + 3 * p.scratch_len;
+    const float* xf = static_cast<const float*>(x) + (size_t)t * p.T * 2;
+    for (int n = 0; n < p.T; ++n) cur[n] = (double)xf[2 * n + comp];
+    float* tab = static_cast<float*>(table) + (size_t)t * p.taps_per_t * 2;
+    for (int s = 1; s <= p.J; ++s) {
+      const long alo = cl_div2(lo + sp.lLo), ahi = fl_div2(hi + sp.lHi);
+      const long blo = cl_div2(lo + sp.hLo), bhi = fl_div2(hi + sp.hHi);
+      const long klo = (alo < blo ? alo : blo) - 2, khi = (ahi > bhi ? ahi : bhi) + 2;
+      analysis_level<double>(p.fam, cur, lo, hi, e, o, klo, khi);
+      const int ti = s - 1;
+      for (int i = 0; i < p.cnt[ti]; ++i) {
+        const long k = p.klo[ti] + i;
+        tab[2 * (p.off[ti] + i) + comp] = (float)o[k - klo];
+      }
+      for (long k = alo; k <= ahi; ++k) nxt[k - alo] = e[k - klo];
+      double* tmp = cur; cur = nxt; nxt = tmp;
+      lo = alo; hi = ahi;
+    }
+    for (int i = 0; i < p.cnt[p.J]; ++i) tab[2 * (p.off[p.J] + i) + comp] = (float)cur[p.klo[p.J] + i - lo];
+  } else {
+    int64_t* cur = reinterpret_cast<int64_t*>(base);
+    int64_t* nxt = cur + p.scratch_len;
+    int64_t* e = cur + 2 * p.scratch_len;
+    int64_t* o = cur + 3 * p.scratch_len;
+    const int16_t* xi = static_cast<const int16_t*>(x) + (size_t)t * p.T * 2;
+    for (int n = 0; n < p.T; ++n) cur[n] = xi[2 * n + comp];
+    int* tab = static_cast<int*>(table) + (size_t)t * p.taps_per_t * 2;
+    for (int s = 1; s <= p.J; ++s) {
+      const long alo = cl_div2(lo + sp.lLo), ahi = fl_div2(hi + sp.lHi);
+      const long blo = cl_div2(lo + sp.hLo), bhi = fl_div2(hi + sp.hHi);
+      const long klo = (alo < blo ? alo : blo) - 2, khi = (ahi > bhi ? ahi : bhi) + 2;
+      analysis_level_int(cur, lo, hi, e, o, klo, khi);
+      const int ti = s - 1;
+      for (int i = 0; i < p.cnt[ti]; ++i) tab[2 * (p.off[ti] + i) + comp] = (int)o[p.klo[ti] + i - klo];
+      for (long k = alo; k <= ahi; ++k) nxt[k - alo] = e[k - klo];
+      int64_t* tmp = cur; cur = nxt; nxt = tmp;
+      lo = alo; hi = ahi;
+    }
+    for (int i = 0; i < p.cnt[p.J]; ++i) tab[2 * (p.off[p.J] + i) + comp] = (int)cur[p.klo[p.J] + i - lo];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: fused multi-level SIDWT lifting of one (row, component, tile).
+//
+// smem: U[lbuf] (in-place working band, fine-grid positions A .. A+lbuf) and
+// Wst[tile_len] (detail staging).  Level s (stride h = 2^{s-1}): thread w owns a
+// run of RV consecutive pairs j0..j0+RV-1 of branch rho = w mod h (fine-grid
+// positions rho + h j), loads RV + HL + HR values, lifts in registers, then
+// (after a barrier) writes U_s in place and W_s into staging; one thread stores
+// the staging plane with a bulk async copy (TMA engine) while the next level
+// computes.  Each input sample is read from HBM once per component; every band
+// byte is written once.  Bank-conflict free: RV odd.
+// ---------------------------------------------------------------------------
+struct AnaParams {
+  int N, J, ext, stride, ML;
+  int tile_len, ntiles, halo_l, lbuf;
+  long long rows;
+};
+
+template <int FAM, int RV>
+__global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_in, void* __restrict__ bands, AnaParams p) {
+  typedef typename Dual<FAM>::T T;
+  constexpr int HL = Dual<FAM>::HL, HR = Dual<FAM>::HR, WIN = RV + HL + HR;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* U = reinterpret_cast<T*>(smem_raw);
+  T* Wst = U + p.lbuf;
+
+  const int tile = blockIdx.x % p.ntiles;
+  const long long rc = blockIdx.x / p.ntiles;
+  const int comp = (int)(rc & 1);
+  const long long row = rc >> 1;
+  const int tstart = tile * p.tile_len;
+  const int out_len = min(p.tile_len, p.stride - tstart);
+  const long long A = (long long)(-p.ML + tstart) - p.halo_l;
+
+  // load the extended row segment (one component)
+  if constexpr (FAM == FI53) {
+    const int16_t* src = static_cast<const int16_t*>(rows_in) + (size_t)row * p.N * 2 + comp;
+    for (int u = threadIdx.x; u < p.lbuf; u += blockDim.x)
+      U[u] = (T)__ldg(src + 2 * (size_t)ext_index(A + u, p.N, p.ext));
+  } else {
+    const float* src = static_cast<const float*>(rows_in) + (size_t)row * p.N * 2 + comp;
+    for (int u = threadIdx.x; u < p.lbuf; u += blockDim.x)
+      U[u] = (T)__ldg(src + 2 * (size_t)ext_index(A + u, p.N, p.ext));
+  }
+  __syncthreads();
+
+  T* plane0 = static_cast<T*>(bands) + ((size_t)row * (p.J + 1) * 2 + comp) * p.stride + tstart;
+  const size_t band_step = (size_t)2 * p.stride;
+
+  for (int s = 1; s <= p.J; ++s) {
+    const int lh = s - 1;
+    const int h = 1 << lh;
+    const int w = threadIdx.x;
+    const int rho = w & (h - 1);
+    const int j0 = (w >> lh) * RV;
+    const int len = (p.lbuf - rho + h - 1) >> lh;   // positions rho + h j < lbuf
+    const bool active = j0 < len;
+    T c[RV], d[RV];
+    if (active) {
+      T v[WIN];
+#pragma unroll
+      for (int i = 0; i < WIN; ++i) {
+        int j = j0 - HL + i;
+        j = max(0, min(j, len - 1));
+        v[i] = U[rho + (j << lh)];
+      }
+      Dual<FAM>::template run<RV>(v, c, d);
+    }
+    if (threadIdx.x == 0 && s > 1) bulk_wait_read_all();   // staging free again
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < RV; ++i) {
+        const int j = j0 + i;
+        if (j < len) {
+          const int u = rho + (j << lh);
+          U[u] = c[i];
+          const int wu = u - p.halo_l;
+          if (wu >= 0 && wu < out_len) Wst[wu] = d[i];
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_store_s2g(plane0 + (size_t)(s - 1) * band_step, Wst, (uint32_t)(out_len * sizeof(T)));
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) {
+    bulk_store_s2g(plane0 + (size_t)p.J * band_step, U + p.halo_l, (uint32_t)(out_len * sizeof(T)));
+    bulk_commit();
+    bulk_wait_all();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Peak partial record (per row, template, scale, lag tile).
+// ---------------------------------------------------------------------------
+struct PeakF { float m2; int tau; float re, im; };
+struct PeakI { unsigned long long m2; int tau; int re, im, pad; };
+
+__device__ __forceinline__ float mag2f(float re, float im) { return __fmaf_rn(re, re, __fmul_rn(im, im)); }
+__device__ __forceinline__ unsigned long long mag2i(int re, int im) {
+  return (unsigned long long)((long long)re * re) + (unsigned long long)((long long)im * im);
+}
+// a beats b: larger magnitude, or equal magnitude and smaller lag
+template <typename M>
+__device__ __forceinline__ bool beats(M ma, int ta, M mb, int tb) { return ma > mb || (ma == mb && ta < tb); }
+
+// ---------------------------------------------------------------------------
+// K2: correlation.  One CTA per (row, template, lag tile of TT).  Terms are taken
+// coarsest first: A_J (band J, stride 2^J), then D_J .. D_1 (band i-1, stride 2^i).
+// After term i the accumulator holds corr_i (eq. (4) suffix sum) and is stored.
+// Per term, thread item (r, qb) computes Q consecutive outputs of residue class r
+// (lags tau = r + g q) as a sliding window over the taps: 4 FFMA (or 4 IMAD) per
+// tap per output, one smem load per tap per item, taps broadcast from smem.
+// ---------------------------------------------------------------------------
+struct Term { int band, lg, kmin, npad, toff; };
+struct CorParams {
+  int N, J, ext, stride, ML, n_t, TT, ntiles, taps_per_t, blen_max;
+  long long rows;
+  int want_corr, want_peaks;
+  Term term[kMaxTerms];
+};
+
+template <bool INT, int Q>
+__device__ __forceinline__ void corr_item(const float* sre, const float* sim, int blen, const float2* tp, int npad,
+                                          int r, int lg, int q0, float (&ar)[Q], float (&ai)[Q]) {
+  float wr[Q], wi[Q];
+#pragma unroll
+  for (int m = 0; m < Q; ++m) {
+    const int x = min(r + ((q0 + m) << lg), blen - 1);
+    wr[m] = sre[x]; wi[m] = sim[x];
+    ar[m] = 0.f; ai[m] = 0.f;
+  }
+  for (int kc = 0; kc < npad; kc += Q) {
+#pragma unroll
+    for (int kk = 0; kk < Q; ++kk) {
+      const float2 t = tp[kc + kk];
+      const float nty = -t.y;
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const int sl = (j + kk) % Q;
+        ar[j] = fmaf(t.x, wr[sl], ar[j]);
+        ar[j] = fmaf(t.y, wi[sl], ar[j]);
+        ai[j] = fmaf(t.x, wi[sl], ai[j]);
+        ai[j] = fmaf(nty, wr[sl], ai[j]);
+      }
+      const int x = min(r + ((q0 + kc + Q + kk) << lg), blen - 1);
+      wr[kk] = sre[x]; wi[kk] = sim[x];
+    }
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void corr_item_int(const int* sre, const int* sim, int blen, const int2* tp, int npad,
+                                              int r, int lg, int q0, unsigned (&ar)[Q], unsigned (&ai)[Q]) {
+  unsigned wr[Q], wi[Q];
+#pragma unroll
+  for (int m = 0; m < Q; ++m) {
+    const int x = min(r + ((q0 + m) << lg), blen - 1);
+    wr[m] = (unsigned)sre[x]; wi[m] = (unsigned)sim[x];
+    ar[m] = 0u; ai[m] = 0u;
+  }
+  for (int kc = 0; kc < npad; kc += Q) {
+#pragma unroll
+    for (int kk = 0; kk < Q; ++kk) {
+      const int2 t = tp[kc + kk];
+      const unsigned tx = (unsigned)t.x, ty = (unsigned)t.y, nty = 0u - ty;
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const int sl = (j + kk) % Q;
+        ar[j] += tx * wr[sl] + ty * wi[sl];          // wrap-around int32 (exact mod 2^32)
+        ai[j] += tx * wi[sl] + nty * wr[sl];
+      }
+      const int x = min(r + ((q0 + kc + Q + kk) << lg), blen - 1);
+      wr[kk] = (unsigned)sre[x]; wi[kk] = (unsigned)sim[x];
+    }
+  }
+}
+
+template <bool INT, int Q>
+__global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
+                                                   void* __restrict__ corr, void* __restrict__ partials, CorParams p) {
+  typedef typename std::conditional<INT, int, float>::type T;
+  typedef typename std::conditional<INT, int2, float2>::type T2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T2* stap = reinterpret_cast<T2*>(smem_raw);
+  T* sre = reinterpret_cast<T*>(stap + p.taps_per_t);
+  T* sim = sre + p.blen_max;
+  T* acc = sim + p.blen_max;                 // [2 buffers][2 planes][TT]
+  constexpr int kWarps = 256 / 32;
+  typedef typename std::conditional<INT, PeakI, PeakF>::type PK;
+  __shared__ PK red[kMaxTerms][kWarps];
+
+  const int tile = blockIdx.x % p.ntiles;
+  const long long bt = blockIdx.x / p.ntiles;
+  const int t = (int)(bt % p.n_t);
+  const long long row = bt / p.n_t;
+  const int tau0 = tile * p.TT;
+  const int TT = p.TT;
+
+  const T2* tsrc = static_cast<const T2*>(taps) + (size_t)t * p.taps_per_t;
+  for (int i = threadIdx.x; i < p.taps_per_t; i += blockDim.x) stap[i] = tsrc[i];
+
+  const T* brow = static_cast<const T*>(bands) + (size_t)row * (p.J + 1) * 2 * p.stride;
+  int cur = 0;
+  for (int step = 0; step <= p.J; ++step) {
+    const int ti = p.J - step;
+    const Term tm = p.term[ti];
+    const int g = 1 << tm.lg;
+    const int blen = TT + g * (tm.npad - 1);
+    const long long pos0 = (long long)tau0 + (long long)g * tm.kmin;
+    const T* pre = brow + (size_t)tm.band * 2 * p.stride;
+    const T* pim = pre + p.stride;
+    for (int xx = threadIdx.x; xx < blen; xx += blockDim.x) {
+      const long long P = pos0 + xx;
+      int idx;
+      if (p.ext == 0) { long long m = P % p.N; idx = (int)(m < 0 ? m + p.N : m); }
+      else { long long q = P + p.ML; idx = (int)(q < 0 ? 0 : (q >= p.stride ? p.stride - 1 : q)); }
+      sre[xx] = __ldg(pre + idx);
+      sim[xx] = __ldg(pim + idx);
+    }
+    __syncthreads();
+    // compute term, accumulate into acc[cur^1] = acc[cur] + term
+    const int nq = TT >> tm.lg;
+    const int nqb = (nq + Q - 1) / Q;
+    T* aprev = acc + (size_t)cur * 2 * TT;
+    T* anew = acc + (size_t)(cur ^ 1) * 2 * TT;
+    for (int w = threadIdx.x; w < g * nqb; w += blockDim.x) {
+      const int r = w & (g - 1);
+      const int q0 = (w >> tm.lg) * Q;
+      if constexpr (INT) {
+        unsigned ar[Q], ai[Q];
+        corr_item_int<Q>(sre, sim, blen, stap + tm.toff, tm.npad, r, tm.lg, q0, ar, ai);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          if (q0 + j < nq) {
+            const int tl = r + ((q0 + j) << tm.lg);
+            const unsigned pr = step ? (unsigned)aprev[tl] : 0u, pi = step ? (unsigned)aprev[TT + tl] : 0u;
+            anew[tl] = (int)(pr + ar[j]);
+            anew[TT + tl] = (int)(pi + ai[j]);
+          }
+        }
+      } else {
+        float ar[Q], ai[Q];
+        corr_item<INT, Q>(sre, sim, blen, stap + tm.toff, tm.npad, r, tm.lg, q0, ar, ai);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          if (q0 + j < nq) {
+            const int tl = r + ((q0 + j) << tm.lg);
+            anew[tl] = (step ? aprev[tl] : 0.f) + ar[j];
+            anew[TT + tl] = (step ? aprev[TT + tl] : 0.f) + ai[j];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+    // store corr_ti and reduce the peak partial of this tile
+    const T* a = acc + (size_t)cur * 2 * TT;
+    T2* dst = p.want_corr ? static_cast<T2*>(corr) + (((size_t)row * p.n_t + t) * (p.J + 1) + ti) * p.N + tau0 : nullptr;
+    PK best;
+    best.m2 = 0; best.tau = 0x7fffffff; best.re = 0; best.im = 0;
+    for (int tl = threadIdx.x; tl < TT; tl += blockDim.x) {
+      T2 v;
+      v.x = a[tl]; v.y = a[TT + tl];
+      if (dst) dst[tl] = v;
+      if (p.want_peaks) {
+        if constexpr (INT) {
+          const unsigned long long m = mag2i(v.x, v.y);
+          if (beats(m, tau0 + tl, best.m2, best.tau) || best.tau == 0x7fffffff) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
+        } else {
+          const float m = mag2f(v.x, v.y);
+          if (beats(m, tau0 + tl, best.m2, best.tau) || best.tau == 0x7fffffff) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
+        }
+      }
+    }
+    if (p.want_peaks) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        PK o;
+        o.m2 = __shfl_down_sync(0xffffffffu, best.m2, off);
+        o.tau = __shfl_down_sync(0xffffffffu, best.tau, off);
+        o.re = __shfl_down_sync(0xffffffffu, best.re, off);
+        o.im = __shfl_down_sync(0xffffffffu, best.im, off);
+        if (o.tau != 0x7fffffff && (best.tau == 0x7fffffff || beats(o.m2, o.tau, best.m2, best.tau))) best = o;
+      }
+      if ((threadIdx.x & 31) == 0) red[ti][threadIdx.x >> 5] = best;
+    }
+  }
+  if (p.want_peaks) {
+    __syncthreads();
+    for (int ti = threadIdx.x; ti <= p.J; ti += blockDim.x) {
+      PK b = red[ti][0];
+      for (int w = 1; w < kWarps; ++w) {
+        const PK o = red[ti][w];
+        if (o.tau != 0x7fffffff && (b.tau == 0x7fffffff || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
+      }
+      static_cast<PK*>(partials)[(((size_t)row * p.n_t + t) * (p.J + 1) + ti) * p.ntiles + tile] = b;
+    }
+  }
+}
+
+// Combine per-tile peak partials (tiles ordered by lag: ties keep the earlier tile).
+template <bool INT>
+__global__ void k_peaks_finalize(const void* __restrict__ partials, int ntiles, long long count,
+                                 int32_t* __restrict__ lag, void* __restrict__ val) {
+  typedef typename std::conditional<INT, PeakI, PeakF>::type PK;
+  typedef typename std::conditional<INT, int2, float2>::type T2;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const PK* pp = static_cast<const PK*>(partials) + (size_t)i * ntiles;
+  PK b = pp[0];
+  for (int k = 1; k < ntiles; ++k) {
+    const PK o = pp[k];
+    if (beats(o.m2, o.tau, b.m2, b.tau)) b = o;
+  }
+  lag[i] = b.tau;
+  if (val) { T2 v; v.x = b.re; v.y = b.im; static_cast<T2*>(val)[i] = v; }
+}
+
+// K3: standalone peak search over a stored correlation [count][N].
+template <bool INT>
+__global__ void __launch_bounds__(256) k_peaks(const void* __restrict__ corr, int N, int32_t* __restrict__ lag,
+                                               void* __restrict__ val) {
+  typedef typename std::conditional<INT, PeakI, PeakF>::type PK;
+  typedef typename std::conditional<INT, int2, float2>::type T2;
+  __shared__ PK red[8];
+  const T2* c = static_cast<const T2*>(corr) + (size_t)blockIdx.x * N;
+  PK best;
+  best.m2 = 0; best.tau = 0x7fffffff; best.re = 0; best.im = 0;
+  for (int tau = threadIdx.x; tau < N; tau += blockDim.x) {
+    const T2 v = c[tau];
+    if constexpr (INT) {
+      const unsigned long long m = mag2i(v.x, v.y);
+      if (best.tau == 0x7fffffff || beats(m, tau, best.m2, best.tau)) { best.m2 = m; best.tau = tau; best.re = v.x; best.im = v.y; }
+    } else {
+      const float m = mag2f(v.x, v.y);
+      if (best.tau == 0x7fffffff || beats(m, tau, best.m2, best.tau)) { best.m2 = m; best.tau = tau; best.re = v.x; best.im = v.y; }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    PK o;
+    o.m2 = __shfl_down_sync(0xffffffffu, best.m2, off);
+    o.tau = __shfl_down_sync(0xffffffffu, best.tau, off);
+    o.re = __shfl_down_sync(0xffffffffu, best.re, off);
+    o.im = __shfl_down_sync(0xffffffffu, best.im, off);
+    if (o.tau != 0x7fffffff && (best.tau == 0x7fffffff || beats(o.m2, o.tau, best.m2, best.tau))) best = o;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    PK b = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      const PK o = red[w];
+      if (o.tau != 0x7fffffff && (b.tau == 0x7fffffff || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
+    }
+    lag[blockIdx.x] = b.tau;
+    if (val) { T2 v; v.x = b.re; v.y = b.im; static_cast<T2*>(val)[blockIdx.x] = v; }
+  }
+}
+
+}  // namespace sidwt

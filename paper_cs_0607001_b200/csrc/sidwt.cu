@@ -1,0 +1,389 @@
+// sidwt.cu -- host side of libsidwt: the C ABI declared in include/sidwt.h.
+// Plans, validation, template loading, layout, and launches of the sm_100a
+// kernels in kernels.cuh.  No computation of the path happens on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/sidwt.h"
+#include "kernels.cuh"
+
+using namespace sidwt;
+
+namespace {
+
+constexpr int kRV = 15;     // K1 run length (odd: bank-conflict free)
+constexpr int kQ = 9;       // K2 outputs per item (odd: bank-conflict free)
+constexpr int kK2Threads = 256;
+
+inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct sidwt_plan_s {
+  int fam = 0, J = 0, ext = 0;
+  int64_t N = 0, batch = 0;
+  bool loaded = false;
+  int T = 0, n_t = 0;
+  // template terms: i < J -> b_{i+1}, i = J -> a_J
+  int kmin[kMaxTerms] = {}, cnt[kMaxTerms] = {}, npad[kMaxTerms] = {}, toff[kMaxTerms] = {};
+  int taps_per_t = 0;
+  int ML = 0, MR = 0;
+  int64_t stride = -1;
+  void* d_taps = nullptr;
+  // K1 configuration
+  AnaParams ana{};
+  int ana_threads = 0;
+  size_t ana_smem = 0;
+  // K2 configuration
+  CorParams cor{};
+  size_t cor_smem = 0;
+  // workspaces
+  void* d_partials = nullptr;
+  size_t partials_bytes = 0;
+  void *w_rows = nullptr, *w_bands = nullptr, *w_corr = nullptr, *w_lag = nullptr, *w_val = nullptr;
+  int last_launches = 0;
+};
+
+static bool is_int(const sidwt_plan_s* p) { return p->fam == SIDWT_LEGALL53_INT; }
+static size_t sample_bytes(const sidwt_plan_s* p) { return is_int(p) ? 4 : 8; }
+
+// Definitions take C linkage from the extern "C" declarations in include/sidwt.h.
+
+const char* sidwt_status_string(sidwt_status st) {
+  switch (st) {
+    case SIDWT_OK: return "ok";
+    case SIDWT_ERR_PARAM: return "parameter error";
+    case SIDWT_ERR_LENGTH: return "length error";
+    case SIDWT_ERR_DIMENSION: return "dimension error";
+    case SIDWT_ERR_DEPTH: return "depth error";
+    case SIDWT_ERR_RANGE: return "range error";
+    case SIDWT_ERR_STATE: return "state error";
+    case SIDWT_ERR_OOM: return "out of device memory";
+    case SIDWT_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t N, int64_t batch, int ext) {
+  if (!out) return SIDWT_ERR_PARAM;
+  *out = nullptr;
+  if (filter < 0 || filter > 3 || (ext != SIDWT_EXT_PERIODIC && ext != SIDWT_EXT_SYMMETRIC)) return SIDWT_ERR_PARAM;
+  if (N < 2 || (N & (N - 1)) != 0) return SIDWT_ERR_PARAM;
+  if (N > (int64_t(1) << 24)) return SIDWT_ERR_RANGE;
+  if (levels < 1 || levels > SIDWT_MAX_LEVELS || (int64_t(1) << levels) > N) return SIDWT_ERR_DEPTH;
+  if (batch < 1) return SIDWT_ERR_DIMENSION;
+  sidwt_plan_s* p = new (std::nothrow) sidwt_plan_s();
+  if (!p) return SIDWT_ERR_OOM;
+  p->fam = filter; p->J = levels; p->N = N; p->batch = batch; p->ext = ext;
+  *out = p;
+  return SIDWT_OK;
+}
+
+static void free_ws(sidwt_plan_s* p) {
+  void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val};
+  for (void** b : bufs) { if (*b) cudaFree(*b); *b = nullptr; }
+  p->partials_bytes = 0;
+}
+
+sidwt_status sidwt_plan_destroy(sidwt_plan plan) {
+  if (!plan) return SIDWT_OK;
+  free_ws(plan);
+  delete plan;
+  return SIDWT_OK;
+}
+
+int64_t sidwt_band_stride(sidwt_plan p) { return (p && p->loaded) ? p->stride : -1; }
+int64_t sidwt_band_offset(sidwt_plan p) { return (p && p->loaded) ? p->ML : -1; }
+int64_t sidwt_bands_bytes(sidwt_plan p, int64_t rows) {
+  if (!p || !p->loaded) return -1;
+  return rows * (p->J + 1) * 2 * p->stride * 4;
+}
+int64_t sidwt_corr_bytes(sidwt_plan p, int64_t rows) {
+  if (!p || !p->loaded) return -1;
+  return rows * p->n_t * (p->J + 1) * p->N * 8;
+}
+int sidwt_last_launches(sidwt_plan p) { return p ? p->last_launches : 0; }
+
+// ---------------------------------------------------------------------------
+// Template load: supports, margins, tiling, and the device pyramid (K0).
+// ---------------------------------------------------------------------------
+static void configure(sidwt_plan_s* p) {
+  const int J = p->J;
+  const Supp sp = analysis_support(p->fam);
+  // supports of the critically sampled pyramid (zero-extended template on [0,T))
+  long lo = 0, hi = p->T - 1;
+  for (int s = 1; s <= J; ++s) {
+    const long alo = cl_div2(lo + sp.lLo), ahi = fl_div2(hi + sp.lHi);
+    const long blo = cl_div2(lo + sp.hLo), bhi = fl_div2(hi + sp.hHi);
+    p->kmin[s - 1] = (int)blo; p->cnt[s - 1] = (int)(bhi - blo + 1);
+    lo = alo; hi = ahi;
+  }
+  p->kmin[J] = (int)lo; p->cnt[J] = (int)(hi - lo + 1);
+  int off = 0;
+  for (int i = 0; i <= J; ++i) {
+    p->npad[i] = (int)rup(p->cnt[i], kQ);
+    p->toff[i] = off;
+    off += p->npad[i];
+  }
+  p->taps_per_t = off;
+  // correlation reach -> band margins (DESIGN.md R-D6 GPU)
+  int ML = 0, MR = 0;
+  for (int i = 0; i <= J; ++i) {
+    const int g = 1 << (i < J ? i + 1 : J);
+    ML = std::max(ML, -g * p->kmin[i]);
+    MR = std::max(MR, g * (p->kmin[i] + p->cnt[i] - 1));
+  }
+  if (p->ext == SIDWT_EXT_PERIODIC) { ML = 0; MR = 0; }
+  p->ML = ML; p->MR = MR;
+  p->stride = rup(ML + p->N + MR, 32);
+
+  // ---- K1 tiling
+  const Reach rc = dual_reach(p->fam);
+  const int maxL = std::max(rc.lowL, rc.hiL);
+  const int64_t halo_l = rup((int64_t)maxL * ((1LL << J) - 1), 4);
+  const int64_t halo_r = std::max<int64_t>((int64_t)rc.lowR * ((1LL << J) - 1),
+                                           (int64_t)rc.lowR * ((1LL << (J - 1)) - 1) + (int64_t)rc.hiR * (1LL << (J - 1)));
+  int64_t lbuf_target = 6144;
+  if (const char* e = std::getenv("SIDWT_K1_LBUF")) lbuf_target = std::max<int64_t>(256, atoll(e));
+  int64_t ntiles = 1, tile_len = 0, lbuf = 0, threads = 0;
+  for (;; ++ntiles) {
+    tile_len = rup(cdiv(p->stride, ntiles), 32);
+    lbuf = rup(halo_l + tile_len + halo_r, 4);
+    threads = 0;
+    for (int s = 1; s <= J; ++s) {
+      const int64_t h = 1LL << (s - 1);
+      threads = std::max(threads, h * cdiv(cdiv(lbuf, h), kRV));
+    }
+    if ((lbuf <= lbuf_target && threads <= 512) || tile_len <= 32) break;
+  }
+  ntiles = cdiv(p->stride, tile_len);
+  p->ana.N = (int)p->N; p->ana.J = J; p->ana.ext = p->ext; p->ana.stride = (int)p->stride; p->ana.ML = ML;
+  p->ana.tile_len = (int)tile_len; p->ana.ntiles = (int)ntiles; p->ana.halo_l = (int)halo_l; p->ana.lbuf = (int)lbuf;
+  p->ana_threads = (int)std::min<int64_t>(512, rup(threads, 32));
+  p->ana_smem = (size_t)(lbuf + tile_len) * 4;
+
+  // ---- K2 tiling
+  int64_t TT = std::min<int64_t>(p->N, std::max<int64_t>(2048, 1LL << J));
+  CorParams& c = p->cor;
+  c.N = (int)p->N; c.J = J; c.ext = p->ext; c.stride = (int)p->stride; c.ML = ML; c.n_t = p->n_t;
+  c.TT = (int)TT; c.ntiles = (int)(p->N / TT); c.taps_per_t = p->taps_per_t;
+  int blen_max = 0;
+  for (int i = 0; i <= J; ++i) {
+    const int lg = i < J ? i + 1 : J;
+    c.term[i].band = i; c.term[i].lg = lg; c.term[i].kmin = p->kmin[i];
+    c.term[i].npad = p->npad[i]; c.term[i].toff = p->toff[i];
+    blen_max = std::max<int>(blen_max, (int)TT + (1 << lg) * (p->npad[i] - 1));
+  }
+  c.blen_max = blen_max;
+  p->cor_smem = (size_t)p->taps_per_t * 8 + (size_t)2 * blen_max * 4 + (size_t)4 * TT * 4;
+}
+
+static sidwt_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return SIDWT_OK;
+  if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); return SIDWT_ERR_OOM; }
+  cudaGetLastError();
+  return SIDWT_ERR_CUDA;
+}
+
+sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64_t T, int n_templates) {
+  if (!p || !host_templates) return SIDWT_ERR_PARAM;
+  if (T < 1 || T > p->N) return SIDWT_ERR_LENGTH;
+  if (n_templates < 1 || n_templates > 65536) return SIDWT_ERR_DIMENSION;
+  if (p->d_taps) { cudaFree(p->d_taps); p->d_taps = nullptr; }
+  if (p->d_partials) { cudaFree(p->d_partials); p->d_partials = nullptr; p->partials_bytes = 0; }
+  p->loaded = false;
+  p->T = (int)T; p->n_t = n_templates;
+  configure(p);
+  if (p->cor_smem > 200 * 1024 || p->ana_smem > 200 * 1024) return SIDWT_ERR_RANGE;
+
+  const size_t tab_bytes = (size_t)n_templates * p->taps_per_t * 8;
+  const size_t x_bytes = (size_t)n_templates * T * sample_bytes(p);
+  PyrParams pp{};
+  pp.fam = p->fam; pp.J = p->J; pp.T = (int)T; pp.n_t = n_templates; pp.taps_per_t = p->taps_per_t;
+  for (int i = 0; i <= p->J; ++i) { pp.klo[i] = p->kmin[i]; pp.cnt[i] = p->cnt[i]; pp.off[i] = p->toff[i]; }
+  pp.scratch_len = (int)T + 64;
+  void* d_x = nullptr;
+  double* d_scr = nullptr;
+  cudaError_t e = cudaMalloc(&p->d_taps, tab_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&d_x, x_bytes);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&d_scr, (size_t)2 * n_templates * 4 * pp.scratch_len * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(p->d_taps, 0, tab_bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(d_x, host_templates, x_bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    const int threads = 64;
+    k_template_pyramid<<<(unsigned)cdiv(2 * n_templates, threads), threads>>>(d_x, p->d_taps, d_scr, pp);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (d_x) cudaFree(d_x);
+  if (d_scr) cudaFree(d_scr);
+  if (e != cudaSuccess) {
+    if (p->d_taps) { cudaFree(p->d_taps); p->d_taps = nullptr; }
+    return cuda_status(e);
+  }
+  p->loaded = true;
+  return SIDWT_OK;
+}
+
+int64_t sidwt_template_taps(sidwt_plan p, void* host_taps, int32_t* kmin, int32_t* count) {
+  if (!p || !p->loaded) return -1;
+  if (kmin) for (int i = 0; i <= p->J; ++i) kmin[i] = p->kmin[i];
+  if (count) for (int i = 0; i <= p->J; ++i) count[i] = p->cnt[i];
+  int64_t per_t = 0;
+  for (int i = 0; i <= p->J; ++i) per_t += p->cnt[i];
+  if (host_taps) {
+    std::vector<uint64_t> tab((size_t)p->n_t * p->taps_per_t);
+    if (cudaMemcpy(tab.data(), p->d_taps, tab.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) { cudaGetLastError(); return -1; }
+    uint64_t* out = static_cast<uint64_t*>(host_taps);
+    for (int t = 0; t < p->n_t; ++t)
+      for (int i = 0; i <= p->J; ++i)
+        for (int k = 0; k < p->cnt[i]; ++k) *out++ = tab[(size_t)t * p->taps_per_t + p->toff[i] + k];
+  }
+  return per_t;
+}
+
+// ---------------------------------------------------------------------------
+// Device calls
+// ---------------------------------------------------------------------------
+template <int FAM>
+static cudaError_t launch_analyze(const sidwt_plan_s* p, const void* rows, int64_t nrows, void* bands, cudaStream_t s) {
+  auto kern = k_analyze<FAM, kRV>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->ana_smem);
+  if (e != cudaSuccess) return e;
+  AnaParams a = p->ana;
+  a.rows = nrows;
+  const int64_t grid = nrows * 2 * a.ntiles;
+  kern<<<(unsigned)grid, p->ana_threads, p->ana_smem, s>>>(rows, bands, a);
+  return cudaGetLastError();
+}
+
+sidwt_status sidwt_analyze(sidwt_plan p, const void* d_rows, int64_t rows, void* d_bands, void* stream) {
+  if (!p || !d_rows || !d_bands) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  if (rows * 2 * p->ana.ntiles > 0x7fffffffLL) return SIDWT_ERR_RANGE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (p->fam) {
+    case F53: e = launch_analyze<F53>(p, d_rows, rows, d_bands, s); break;
+    case F97: e = launch_analyze<F97>(p, d_rows, rows, d_bands, s); break;
+    case FD4: e = launch_analyze<FD4>(p, d_rows, rows, d_bands, s); break;
+    default:  e = launch_analyze<FI53>(p, d_rows, rows, d_bands, s); break;
+  }
+  p->last_launches = 1;
+  return cuda_status(e);
+}
+
+static sidwt_status ensure_partials(sidwt_plan_s* p) {
+  const size_t rec = is_int(p) ? sizeof(PeakI) : sizeof(PeakF);
+  const size_t need = (size_t)p->batch * p->n_t * (p->J + 1) * p->cor.ntiles * rec;
+  if (p->partials_bytes >= need) return SIDWT_OK;
+  if (p->d_partials) cudaFree(p->d_partials);
+  p->d_partials = nullptr;
+  p->partials_bytes = 0;
+  cudaError_t e = cudaMalloc(&p->d_partials, need);
+  if (e != cudaSuccess) return cuda_status(e);
+  p->partials_bytes = need;
+  return SIDWT_OK;
+}
+
+static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
+                                   int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
+  CorParams c = p->cor;
+  c.rows = rows;
+  c.want_corr = d_corr != nullptr;
+  c.want_peaks = peaks;
+  const int64_t grid = rows * p->n_t * c.ntiles;
+  if (grid > 0x7fffffffLL) return SIDWT_ERR_RANGE;
+  cudaError_t e;
+  if (is_int(p)) {
+    auto kern = k_correlate<true, kQ>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cor_smem);
+    if (e == cudaSuccess) {
+      kern<<<(unsigned)grid, kK2Threads, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
+      e = cudaGetLastError();
+    }
+  } else {
+    auto kern = k_correlate<false, kQ>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cor_smem);
+    if (e == cudaSuccess) {
+      kern<<<(unsigned)grid, kK2Threads, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
+      e = cudaGetLastError();
+    }
+  }
+  p->last_launches = 1;
+  if (e == cudaSuccess && peaks) {
+    const int64_t count = rows * p->n_t * (p->J + 1);
+    const unsigned blocks = (unsigned)cdiv(count, 256);
+    if (is_int(p)) k_peaks_finalize<true><<<blocks, 256, 0, s>>>(p->d_partials, c.ntiles, count, d_lag, d_val);
+    else k_peaks_finalize<false><<<blocks, 256, 0, s>>>(p->d_partials, c.ntiles, count, d_lag, d_val);
+    e = cudaGetLastError();
+    p->last_launches = 2;
+  }
+  return cuda_status(e);
+}
+
+sidwt_status sidwt_correlate(sidwt_plan p, const void* d_bands, int64_t rows, void* d_corr, void* stream) {
+  if (!p || !d_bands || !d_corr) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  return correlate_impl(p, d_bands, rows, d_corr, nullptr, nullptr, false, static_cast<cudaStream_t>(stream));
+}
+
+sidwt_status sidwt_correlate_peaks(sidwt_plan p, const void* d_bands, int64_t rows, void* d_corr, int32_t* d_lag,
+                                   void* d_val, void* stream) {
+  if (!p || !d_bands || !d_lag) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  sidwt_status st = ensure_partials(p);
+  if (st != SIDWT_OK) return st;
+  return correlate_impl(p, d_bands, rows, d_corr, d_lag, d_val, true, static_cast<cudaStream_t>(stream));
+}
+
+sidwt_status sidwt_peaks(sidwt_plan p, const void* d_corr, int64_t rows, int32_t* d_lag, void* d_val, void* stream) {
+  if (!p || !d_corr || !d_lag) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  const int64_t count = rows * p->n_t * (p->J + 1);
+  if (count > 0x7fffffffLL) return SIDWT_ERR_RANGE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (is_int(p)) k_peaks<true><<<(unsigned)count, 256, 0, s>>>(d_corr, (int)p->N, d_lag, d_val);
+  else k_peaks<false><<<(unsigned)count, 256, 0, s>>>(d_corr, (int)p->N, d_lag, d_val);
+  p->last_launches = 1;
+  return cuda_status(cudaGetLastError());
+}
+
+sidwt_status sidwt_execute_host(sidwt_plan p, const void* h_rows, int64_t rows, int32_t* h_lag, void* h_val,
+                                void* stream) {
+  if (!p || !h_rows || !h_lag) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  cudaError_t e = cudaSuccess;
+  const size_t cnt = (size_t)p->batch * p->n_t * (p->J + 1);
+  if (!p->w_rows) e = cudaMalloc(&p->w_rows, (size_t)p->batch * p->N * sample_bytes(p));
+  if (e == cudaSuccess && !p->w_bands) e = cudaMalloc(&p->w_bands, (size_t)sidwt_bands_bytes(p, p->batch));
+  if (e == cudaSuccess && !p->w_corr) e = cudaMalloc(&p->w_corr, (size_t)sidwt_corr_bytes(p, p->batch));
+  if (e == cudaSuccess && !p->w_lag) e = cudaMalloc(&p->w_lag, cnt * 4);
+  if (e == cudaSuccess && !p->w_val) e = cudaMalloc(&p->w_val, cnt * 8);
+  if (e != cudaSuccess) return cuda_status(e);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  e = cudaMemcpyAsync(p->w_rows, h_rows, (size_t)rows * p->N * sample_bytes(p), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  sidwt_status st = sidwt_analyze(p, p->w_rows, rows, p->w_bands, stream);
+  if (st != SIDWT_OK) return st;
+  st = sidwt_correlate_peaks(p, p->w_bands, rows, p->w_corr, static_cast<int32_t*>(p->w_lag), p->w_val, stream);
+  if (st != SIDWT_OK) return st;
+  const size_t n = (size_t)rows * p->n_t * (p->J + 1);
+  e = cudaMemcpyAsync(h_lag, p->w_lag, n * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && h_val) e = cudaMemcpyAsync(h_val, p->w_val, n * 8, cudaMemcpyDeviceToHost, s);
+  p->last_launches = 3;
+  return cuda_status(e);
+}
+

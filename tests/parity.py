@@ -1,0 +1,90 @@
+"""Parity helpers: run the CUDA path through the C ABI and compare with the oracle.
+
+Tolerances (BASELINE.json north star; DESIGN.md section "Parity"):
+  fp32 bands      : relative L2 per (row, band) <= 1e-5 vs the oracle's fp64
+  fp32 corr       : max_tau |gpu - oracle| <= 1e-4 x max_tau |oracle| per (row, template, scale)
+  lags (fp32)     : equal to the oracle's argmax, else accepted only as a near tie
+                    |oracle[gpu lag]| >= |oracle[oracle lag]| - 2 tol, counted
+  integer family  : bands, corr, lags and values bit-exact
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle as O
+
+BAND_RTOL = 1e-5
+CORR_TOL = 1e-4
+
+
+def run_gpu(plan, rows: np.ndarray, fused: bool = False):
+    import torch
+    n = rows.shape[0]
+    d_rows = plan.rows_to_device(rows)
+    bands = plan.analyze(d_rows, n)
+    if fused:
+        corr, lag, val = plan.correlate_peaks(bands, n)
+    else:
+        corr = plan.correlate(bands, n)
+        lag, val = plan.peaks(corr, n)
+    torch.cuda.synchronize()
+    out = dict(bands=bands.cpu().numpy(), corr=corr.cpu().numpy(), lag=lag.cpu().numpy(), val=val.cpu().numpy())
+    return out
+
+
+def oracle_for(plan, rows, templates, corr=True, nthreads=0):
+    ML, S = plan.band_offset, plan.band_stride
+    return O.run(plan.filter, plan.levels, plan.ext, plan.N, rows, templates, p_lo=-ML, p_hi=S - ML,
+                 corr=corr, nthreads=nthreads)
+
+
+def compare(plan, g, r, row_ids=None, check_bands=True):
+    """Assert parity of gpu result g (possibly for a superset of rows) with oracle r.
+    Returns stats dict."""
+    J = plan.levels
+    stats = dict(band_rel_l2=0.0, corr_err=0.0, lag_exact=0, lag_neartie=0)
+    gb, gc, gl, gv = g["bands"], g["corr"], g["lag"], g["val"]
+    if row_ids is not None:
+        gb, gc, gl, gv = gb[row_ids], gc[row_ids], gl[row_ids], gv[row_ids]
+    if plan.is_int:
+        if check_bands:
+            ob = r["bands"]                               # [rows][J+1][nb][2] int64
+            gbb = np.stack([gb[:, :, 0, :], gb[:, :, 1, :]], axis=-1).astype(np.int64)
+            assert np.array_equal(gbb, ob), "integer bands differ"
+        assert np.array_equal(gc, r["corr"]), "integer corr differs"
+        assert np.array_equal(gl, r["lag"]), "integer lags differ"
+        assert np.array_equal(gv, r["val"]), "integer peak values differ"
+        stats["lag_exact"] = gl.size
+        return stats
+    if check_bands:
+        ob = r["bands"]                                   # [rows][J+1][nb] complex
+        gbc = gb[:, :, 0, :].astype(np.float64) + 1j * gb[:, :, 1, :]
+        num = np.sqrt((np.abs(gbc - ob) ** 2).sum(-1))
+        den = np.sqrt((np.abs(ob) ** 2).sum(-1))
+        rel = np.where(den > 0, num / np.maximum(den, 1e-300), num)
+        stats["band_rel_l2"] = float(rel.max())
+        assert rel.max() <= BAND_RTOL, f"band rel L2 {rel.max():.3e} > {BAND_RTOL}"
+    oc = r["corr"]
+    gcc = gc[..., 0].astype(np.float64) + 1j * gc[..., 1]
+    peak = np.abs(oc).max(-1)
+    err = np.abs(gcc - oc).max(-1)
+    scaled = np.where(peak > 0, err / np.maximum(peak, 1e-300), err)
+    stats["corr_err"] = float(scaled.max())
+    assert scaled.max() <= CORR_TOL, f"corr max|err|/peak {scaled.max():.3e} > {CORR_TOL}"
+    ol = r["lag"]
+    same = gl == ol
+    stats["lag_exact"] = int(same.sum())
+    if not same.all():
+        idx = np.argwhere(~same)
+        for i in idx:
+            i = tuple(i)
+            tol = CORR_TOL * peak[i]
+            a = np.abs(oc[i][gl[i]])
+            b = np.abs(oc[i][ol[i]])
+            assert a >= b - 2 * tol, f"lag mismatch at {i}: gpu {gl[i]} oracle {ol[i]}"
+            stats["lag_neartie"] += 1
+    # peak values: value of the GPU's corr at the GPU's lag
+    gvc = gv[..., 0] + 1j * gv[..., 1]
+    picked = np.take_along_axis(gcc, gl[..., None].astype(np.int64), -1)[..., 0]
+    assert np.allclose(gvc, picked, rtol=0, atol=0), "peak value is not corr[lag]"
+    return stats
