@@ -34,16 +34,14 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // Extension of the received row (DESIGN.md R-D6): periodic or whole-sample symmetric.
-__device__ __forceinline__ int ext_index(long long n, int N, int ext) {
-  if (ext == 0) {
-    long long m = n % N;
-    return (int)(m < 0 ? m + N : m);
-  }
+// General form (any n); the kernels use a branch-only fast path when the range allows.
+__device__ __forceinline__ int ext_index(int n, int N, int ext) {
+  if (ext == 0) return n & (N - 1);                 // N is a power of two
   if (N == 1) return 0;
-  const long long P = 2LL * N - 2;
-  long long m = n % P;
+  const int P = 2 * N - 2;
+  int m = n % P;
   if (m < 0) m += P;
-  return (int)(m < N ? m : P - m);
+  return m < N ? m : P - m;
 }
 
 // ---------------------------------------------------------------------------
@@ -193,15 +191,52 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
   const int out_len = min(p.tile_len, p.stride - tstart);
   const long long A = (long long)(-p.ML + tstart) - p.halo_l;
 
-  // load the extended row segment (one component)
-  if constexpr (FAM == FI53) {
-    const int16_t* src = static_cast<const int16_t*>(rows_in) + (size_t)row * p.N * 2 + comp;
-    for (int u = threadIdx.x; u < p.lbuf; u += blockDim.x)
-      U[u] = (T)__ldg(src + 2 * (size_t)ext_index(A + u, p.N, p.ext));
-  } else {
-    const float* src = static_cast<const float*>(rows_in) + (size_t)row * p.N * 2 + comp;
-    for (int u = threadIdx.x; u < p.lbuf; u += blockDim.x)
-      U[u] = (T)__ldg(src + 2 * (size_t)ext_index(A + u, p.N, p.ext));
+  // load the extended row segment (one component); 8 independent loads in flight per thread
+  {
+    const int N = p.N;
+    const long long A_hi = A + p.lbuf - 1;
+    const bool fast = (p.ext == 0) ? (A >= -N && A_hi < 2LL * N) : (A >= -(N - 1) && A_hi <= 2LL * N - 2);
+    const int Ai = (int)A;
+    auto src_index = [&](int u) -> int {
+      const int n = Ai + u;
+      if (fast) {
+        if (p.ext == 0) return n < 0 ? n + N : (n >= N ? n - N : n);
+        return n < 0 ? -n : (n >= N ? 2 * N - 2 - n : n);
+      }
+      return ext_index(n, N, p.ext);
+    };
+    constexpr int B = 8;
+    if constexpr (FAM == FI53) {
+      const int16_t* src = static_cast<const int16_t*>(rows_in) + (size_t)row * p.N * 2 + comp;
+      for (int u0 = threadIdx.x; u0 < p.lbuf; u0 += B * blockDim.x) {
+        T v[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          const int u = u0 + k * blockDim.x;
+          v[k] = u < p.lbuf ? (T)__ldg(src + 2 * (size_t)src_index(u)) : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          const int u = u0 + k * blockDim.x;
+          if (u < p.lbuf) U[u] = v[k];
+        }
+      }
+    } else {
+      const float* src = static_cast<const float*>(rows_in) + (size_t)row * p.N * 2 + comp;
+      for (int u0 = threadIdx.x; u0 < p.lbuf; u0 += B * blockDim.x) {
+        T v[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          const int u = u0 + k * blockDim.x;
+          v[k] = u < p.lbuf ? __ldg(src + 2 * (size_t)src_index(u)) : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+          const int u = u0 + k * blockDim.x;
+          if (u < p.lbuf) U[u] = v[k];
+        }
+      }
+    }
   }
   __syncthreads();
 
@@ -270,75 +305,119 @@ template <typename M>
 __device__ __forceinline__ bool beats(M ma, int ta, M mb, int tb) { return ma > mb || (ma == mb && ta < tb); }
 
 // ---------------------------------------------------------------------------
+// mbarrier + bulk async copy global -> shared (TMA engine, SASS UBLKCP.S.G).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // K2: correlation.  One CTA per (row, template, lag tile of TT).  Terms are taken
 // coarsest first: A_J (band J, stride 2^J), then D_J .. D_1 (band i-1, stride 2^i).
 // After term i the accumulator holds corr_i (eq. (4) suffix sum) and is stored.
 // Per term, thread item (r, qb) computes Q consecutive outputs of residue class r
 // (lags tau = r + g q) as a sliding window over the taps: 4 FFMA (or 4 IMAD) per
-// tap per output, one smem load per tap per item, taps broadcast from smem.
+// tap per output, one smem load pair per tap per item, taps broadcast from smem.
+// Band tiles are double buffered: the next term's tile is fetched by two bulk
+// async copies (TMA engine, mbarrier completion) while the current term computes
+// (symmetric extension: contiguous ranges); periodic bands wrap and use batched
+// cooperative loads instead.
 // ---------------------------------------------------------------------------
 struct Term { int band, lg, kmin, npad, toff; };
 struct CorParams {
-  int N, J, ext, stride, ML, n_t, TT, ntiles, taps_per_t, blen_max;
+  int N, J, ext, stride, ML, n_t, TT, ntiles, taps_per_t, balloc, nbuf;
   long long rows;
   int want_corr, want_peaks;
   Term term[kMaxTerms];
 };
 
-template <bool INT, int Q>
-__device__ __forceinline__ void corr_item(const float* sre, const float* sim, int blen, const float2* tp, int npad,
-                                          int r, int lg, int q0, float (&ar)[Q], float (&ai)[Q]) {
-  float wr[Q], wi[Q];
+template <typename T2, int Q, bool LAST>
+__device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int plane, int g, const T2* __restrict__ tp,
+                                             float (&wr)[Q], float (&wi)[Q], float (&ar)[Q], float (&ai)[Q]) {
 #pragma unroll
-  for (int m = 0; m < Q; ++m) {
-    const int x = min(r + ((q0 + m) << lg), blen - 1);
-    wr[m] = sre[x]; wi[m] = sim[x];
-    ar[m] = 0.f; ai[m] = 0.f;
-  }
-  for (int kc = 0; kc < npad; kc += Q) {
+  for (int kk = 0; kk < Q; ++kk) {
+    const float2 t = tp[kk];
+    const float nty = -t.y;
 #pragma unroll
-    for (int kk = 0; kk < Q; ++kk) {
-      const float2 t = tp[kc + kk];
-      const float nty = -t.y;
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        const int sl = (j + kk) % Q;
-        ar[j] = fmaf(t.x, wr[sl], ar[j]);
-        ar[j] = fmaf(t.y, wi[sl], ar[j]);
-        ai[j] = fmaf(t.x, wi[sl], ai[j]);
-        ai[j] = fmaf(nty, wr[sl], ai[j]);
-      }
-      const int x = min(r + ((q0 + kc + Q + kk) << lg), blen - 1);
-      wr[kk] = sre[x]; wi[kk] = sim[x];
+    for (int j = 0; j < Q; ++j) {
+      const int sl = (j + kk) % Q;
+      ar[j] = fmaf(t.x, wr[sl], ar[j]);
+      ar[j] = fmaf(t.y, wi[sl], ar[j]);
+      ai[j] = fmaf(t.x, wi[sl], ai[j]);
+      ai[j] = fmaf(nty, wr[sl], ai[j]);
+    }
+    if (!LAST || kk < Q - 1) {      // the last step's replacement is never consumed
+      const float* q = pr + kk * g;
+      wr[kk] = q[0];
+      wi[kk] = q[plane];
     }
   }
 }
 
-template <int Q>
-__device__ __forceinline__ void corr_item_int(const int* sre, const int* sim, int blen, const int2* tp, int npad,
-                                              int r, int lg, int q0, unsigned (&ar)[Q], unsigned (&ai)[Q]) {
-  unsigned wr[Q], wi[Q];
+template <typename T2, int Q, bool LAST>
+__device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int plane, int g, const T2* __restrict__ tp,
+                                             unsigned (&wr)[Q], unsigned (&wi)[Q], unsigned (&ar)[Q], unsigned (&ai)[Q]) {
 #pragma unroll
-  for (int m = 0; m < Q; ++m) {
-    const int x = min(r + ((q0 + m) << lg), blen - 1);
-    wr[m] = (unsigned)sre[x]; wi[m] = (unsigned)sim[x];
-    ar[m] = 0u; ai[m] = 0u;
-  }
-  for (int kc = 0; kc < npad; kc += Q) {
+  for (int kk = 0; kk < Q; ++kk) {
+    const int2 t = tp[kk];
+    const unsigned tx = (unsigned)t.x, ty = (unsigned)t.y, nty = 0u - ty;
 #pragma unroll
-    for (int kk = 0; kk < Q; ++kk) {
-      const int2 t = tp[kc + kk];
-      const unsigned tx = (unsigned)t.x, ty = (unsigned)t.y, nty = 0u - ty;
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        const int sl = (j + kk) % Q;
-        ar[j] += tx * wr[sl] + ty * wi[sl];          // wrap-around int32 (exact mod 2^32)
-        ai[j] += tx * wi[sl] + nty * wr[sl];
-      }
-      const int x = min(r + ((q0 + kc + Q + kk) << lg), blen - 1);
-      wr[kk] = (unsigned)sre[x]; wi[kk] = (unsigned)sim[x];
+    for (int j = 0; j < Q; ++j) {
+      const int sl = (j + kk) % Q;
+      ar[j] += tx * wr[sl] + ty * wi[sl];            // wrap-around int32 (exact mod 2^32)
+      ai[j] += tx * wi[sl] + nty * wr[sl];
+    }
+    if (!LAST || kk < Q - 1) {      // the last step's replacement is never consumed
+      const int* q = pr + kk * g;
+      wr[kk] = (unsigned)q[0];
+      wi[kk] = (unsigned)q[plane];
     }
   }
+}
+
+// One item: Q outputs q0..q0+Q-1 of residue r; band tile value for output q, tap k' at
+// sb[r + g (q + k')] (re plane) and sb[... + plane] (im plane).  No index clamps: the
+// tile holds every value the valid outputs need; outputs past the residue's end (the
+// ragged last q-block) read at most g (Q-1) values past the tile, inside the buffer.
+template <bool INT, int Q>
+__device__ __forceinline__ void corr_item(const typename std::conditional<INT, int, float>::type* sb, int plane,
+                                          const typename std::conditional<INT, int2, float2>::type* tp, int npad,
+                                          int r, int lg, int q0,
+                                          typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
+                                          typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
+  typedef typename std::conditional<INT, unsigned, float>::type A;
+  const int g = 1 << lg;
+  A wr[Q], wi[Q];
+  const auto* base = sb + r + (q0 << lg);
+#pragma unroll
+  for (int m = 0; m < Q; ++m) {
+    wr[m] = (A)base[m << lg];
+    wi[m] = (A)base[(m << lg) + plane];
+    ar[m] = A(0);
+    ai[m] = A(0);
+  }
+  const auto* pr = base + (Q << lg);
+  int kc = 0;
+  for (; kc + Q < npad; kc += Q, pr += Q * g) {
+    if constexpr (INT) corr_chunk_i<int2, Q, false>(pr, plane, g, tp + kc, wr, wi, ar, ai);
+    else corr_chunk_f<float2, Q, false>(pr, plane, g, tp + kc, wr, wi, ar, ai);
+  }
+  if constexpr (INT) corr_chunk_i<int2, Q, true>(pr, plane, g, tp + kc, wr, wi, ar, ai);
+  else corr_chunk_f<float2, Q, true>(pr, plane, g, tp + kc, wr, wi, ar, ai);
 }
 
 template <bool INT, int Q>
@@ -346,11 +425,12 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
                                                    void* __restrict__ corr, void* __restrict__ partials, CorParams p) {
   typedef typename std::conditional<INT, int, float>::type T;
   typedef typename std::conditional<INT, int2, float2>::type T2;
+  typedef typename std::conditional<INT, unsigned, float>::type A;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T2* stap = reinterpret_cast<T2*>(smem_raw);
-  T* sre = reinterpret_cast<T*>(stap + p.taps_per_t);
-  T* sim = sre + p.blen_max;
-  T* acc = sim + p.blen_max;                 // [2 buffers][2 planes][TT]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);                 // [2]
+  T2* stap = reinterpret_cast<T2*>(smem_raw + 16);
+  T* sbuf = reinterpret_cast<T*>(smem_raw + 16 + (((size_t)p.taps_per_t * sizeof(T2) + 127) & ~(size_t)127));  // [2][2][balloc]
+  T* acc = sbuf + 2 * (size_t)p.nbuf * p.balloc;                          // [2 buffers][2 planes][TT]
   constexpr int kWarps = 256 / 32;
   typedef typename std::conditional<INT, PeakI, PeakF>::type PK;
   __shared__ PK red[kMaxTerms][kWarps];
@@ -361,29 +441,71 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
   const long long row = bt / p.n_t;
   const int tau0 = tile * p.TT;
   const int TT = p.TT;
+  const int plane = p.balloc;
+  const bool tma = (p.ext != 0);
+  const T* brow = static_cast<const T*>(bands) + (size_t)row * (p.J + 1) * 2 * p.stride;
 
+  // tile of term `ti` starts at band index a (symmetric: pos + ML >= 0, always in range)
+  auto issue = [&](int step, int b) {
+    const Term tm = p.term[p.J - step];
+    const int g = 1 << tm.lg;
+    const int blen = TT + g * (tm.npad - 1);
+    const int a = tau0 + g * tm.kmin + p.ML;
+    const int a4 = a & ~3;
+    const uint32_t bytes = (uint32_t)(((a - a4) + blen + 3) & ~3) * 4u;
+    const T* src = brow + (size_t)tm.band * 2 * p.stride + a4;
+    T* dst = sbuf + (size_t)b * 2 * p.balloc;
+    mbar_expect_tx(&mbar[b], 2 * bytes);
+    bulk_load_g2s(dst, src, bytes, &mbar[b]);
+    bulk_load_g2s(dst + p.balloc, src + p.stride, bytes, &mbar[b]);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   const T2* tsrc = static_cast<const T2*>(taps) + (size_t)t * p.taps_per_t;
   for (int i = threadIdx.x; i < p.taps_per_t; i += blockDim.x) stap[i] = tsrc[i];
+  __syncthreads();
+  if (tma && threadIdx.x == 0) issue(0, 0);
+  const bool dbl = p.nbuf == 2;
 
-  const T* brow = static_cast<const T*>(bands) + (size_t)row * (p.J + 1) * 2 * p.stride;
   int cur = 0;
   for (int step = 0; step <= p.J; ++step) {
     const int ti = p.J - step;
     const Term tm = p.term[ti];
     const int g = 1 << tm.lg;
-    const int blen = TT + g * (tm.npad - 1);
-    const long long pos0 = (long long)tau0 + (long long)g * tm.kmin;
-    const T* pre = brow + (size_t)tm.band * 2 * p.stride;
-    const T* pim = pre + p.stride;
-    for (int xx = threadIdx.x; xx < blen; xx += blockDim.x) {
-      const long long P = pos0 + xx;
-      int idx;
-      if (p.ext == 0) { long long m = P % p.N; idx = (int)(m < 0 ? m + p.N : m); }
-      else { long long q = P + p.ML; idx = (int)(q < 0 ? 0 : (q >= p.stride ? p.stride - 1 : q)); }
-      sre[xx] = __ldg(pre + idx);
-      sim[xx] = __ldg(pim + idx);
+    const int b = dbl ? (step & 1) : 0;
+    T* sb = sbuf + (size_t)b * 2 * p.balloc;
+    if (tma) {
+      // double buffer: prefetch the next term now; single buffer: after this compute
+      if (dbl && threadIdx.x == 0 && step < p.J) issue(step + 1, b ^ 1);
+      mbar_wait(&mbar[b], (uint32_t)(dbl ? ((step >> 1) & 1) : (step & 1)));
+      const int a = tau0 + g * tm.kmin + p.ML;
+      sb += (a & 3);
+    } else {
+      // periodic: wrapped positions, batched cooperative loads (8 in flight per thread)
+      const int blen = TT + g * (tm.npad - 1);
+      const int pos0 = tau0 + g * tm.kmin;
+      const T* pre = brow + (size_t)tm.band * 2 * p.stride;
+      for (int x0 = threadIdx.x; x0 < blen; x0 += 8 * blockDim.x) {
+        T vr[8], vi[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int xx = x0 + k * blockDim.x;
+          const int idx = (pos0 + xx) & (p.N - 1);
+          vr[k] = xx < blen ? __ldg(pre + idx) : T(0);
+          vi[k] = xx < blen ? __ldg(pre + p.stride + idx) : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int xx = x0 + k * blockDim.x;
+          if (xx < blen) { sb[xx] = vr[k]; sb[plane + xx] = vi[k]; }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
     // compute term, accumulate into acc[cur^1] = acc[cur] + term
     const int nq = TT >> tm.lg;
     const int nqb = (nq + Q - 1) / Q;
@@ -392,32 +514,20 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
     for (int w = threadIdx.x; w < g * nqb; w += blockDim.x) {
       const int r = w & (g - 1);
       const int q0 = (w >> tm.lg) * Q;
-      if constexpr (INT) {
-        unsigned ar[Q], ai[Q];
-        corr_item_int<Q>(sre, sim, blen, stap + tm.toff, tm.npad, r, tm.lg, q0, ar, ai);
+      A ar[Q], ai[Q];
+      corr_item<INT, Q>(sb, plane, stap + tm.toff, tm.npad, r, tm.lg, q0, ar, ai);
 #pragma unroll
-        for (int j = 0; j < Q; ++j) {
-          if (q0 + j < nq) {
-            const int tl = r + ((q0 + j) << tm.lg);
-            const unsigned pr = step ? (unsigned)aprev[tl] : 0u, pi = step ? (unsigned)aprev[TT + tl] : 0u;
-            anew[tl] = (int)(pr + ar[j]);
-            anew[TT + tl] = (int)(pi + ai[j]);
-          }
-        }
-      } else {
-        float ar[Q], ai[Q];
-        corr_item<INT, Q>(sre, sim, blen, stap + tm.toff, tm.npad, r, tm.lg, q0, ar, ai);
-#pragma unroll
-        for (int j = 0; j < Q; ++j) {
-          if (q0 + j < nq) {
-            const int tl = r + ((q0 + j) << tm.lg);
-            anew[tl] = (step ? aprev[tl] : 0.f) + ar[j];
-            anew[TT + tl] = (step ? aprev[TT + tl] : 0.f) + ai[j];
-          }
+      for (int j = 0; j < Q; ++j) {
+        if (q0 + j < nq) {
+          const int tl = r + ((q0 + j) << tm.lg);
+          const A pr = step ? (A)aprev[tl] : A(0), pi = step ? (A)aprev[TT + tl] : A(0);
+          anew[tl] = (T)(pr + ar[j]);
+          anew[TT + tl] = (T)(pi + ai[j]);
         }
       }
     }
     __syncthreads();
+    if (tma && !dbl && threadIdx.x == 0 && step < p.J) issue(step + 1, 0);
     cur ^= 1;
     // store corr_ti and reduce the peak partial of this tile
     const T* a = acc + (size_t)cur * 2 * TT;
@@ -431,10 +541,10 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
       if (p.want_peaks) {
         if constexpr (INT) {
           const unsigned long long m = mag2i(v.x, v.y);
-          if (beats(m, tau0 + tl, best.m2, best.tau) || best.tau == 0x7fffffff) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
+          if (best.tau == 0x7fffffff || beats(m, tau0 + tl, best.m2, best.tau)) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
         } else {
           const float m = mag2f(v.x, v.y);
-          if (beats(m, tau0 + tl, best.m2, best.tau) || best.tau == 0x7fffffff) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
+          if (best.tau == 0x7fffffff || beats(m, tau0 + tl, best.m2, best.tau)) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
         }
       }
     }

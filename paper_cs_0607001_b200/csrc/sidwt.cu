@@ -133,12 +133,13 @@ static void configure(sidwt_plan_s* p) {
     off += p->npad[i];
   }
   p->taps_per_t = off;
-  // correlation reach -> band margins (DESIGN.md R-D6 GPU)
+  // correlation reach -> band margins (DESIGN.md R-D6 GPU).  The right margin covers the
+  // Q-padded tap range too, so every band value K2 touches exists (no clamps).
   int ML = 0, MR = 0;
   for (int i = 0; i <= J; ++i) {
     const int g = 1 << (i < J ? i + 1 : J);
     ML = std::max(ML, -g * p->kmin[i]);
-    MR = std::max(MR, g * (p->kmin[i] + p->cnt[i] - 1));
+    MR = std::max(MR, g * (p->kmin[i] + p->npad[i] - 1));
   }
   if (p->ext == SIDWT_EXT_PERIODIC) { ML = 0; MR = 0; }
   p->ML = ML; p->MR = MR;
@@ -170,7 +171,9 @@ static void configure(sidwt_plan_s* p) {
   p->ana_smem = (size_t)(lbuf + tile_len) * 4;
 
   // ---- K2 tiling
-  int64_t TT = std::min<int64_t>(p->N, std::max<int64_t>(2048, 1LL << J));
+  int64_t tt_target = 2048;
+  if (const char* e = std::getenv("SIDWT_K2_TT")) tt_target = std::max<int64_t>(64, atoll(e));
+  int64_t TT = std::min<int64_t>(p->N, std::max<int64_t>(tt_target, 1LL << J));
   CorParams& c = p->cor;
   c.N = (int)p->N; c.J = J; c.ext = p->ext; c.stride = (int)p->stride; c.ML = ML; c.n_t = p->n_t;
   c.TT = (int)TT; c.ntiles = (int)(p->N / TT); c.taps_per_t = p->taps_per_t;
@@ -179,10 +182,14 @@ static void configure(sidwt_plan_s* p) {
     const int lg = i < J ? i + 1 : J;
     c.term[i].band = i; c.term[i].lg = lg; c.term[i].kmin = p->kmin[i];
     c.term[i].npad = p->npad[i]; c.term[i].toff = p->toff[i];
-    blen_max = std::max<int>(blen_max, (int)TT + (1 << lg) * (p->npad[i] - 1));
+    blen_max = std::max<int>(blen_max, (int)TT + (1 << lg) * (p->npad[i] - 1 + kQ - 1));
   }
-  c.blen_max = blen_max;
-  p->cor_smem = (size_t)p->taps_per_t * 8 + (size_t)2 * blen_max * 4 + (size_t)4 * TT * 4;
+  c.balloc = (int)rup(blen_max + 4, 4);          // + alignment shift of the bulk copy
+  // double-buffered band tiles when they fit (prefetch overlaps compute), else single
+  c.nbuf = 2;
+  auto smem = [&](int nb) { return 16 + rup((int64_t)p->taps_per_t * 8, 128) + (size_t)2 * nb * c.balloc * 4 + (size_t)4 * TT * 4; };
+  if (smem(2) > 150 * 1024) c.nbuf = 1;
+  p->cor_smem = smem(c.nbuf);
 }
 
 static sidwt_status cuda_status(cudaError_t e) {
