@@ -337,7 +337,7 @@ __device__ __forceinline__ void bulk_load_g2s(void* sdst, const void* gsrc, uint
 // (symmetric extension: contiguous ranges); periodic bands wrap and use batched
 // cooperative loads instead.
 // ---------------------------------------------------------------------------
-struct Term { int band, lg, kmin, npad, toff; };
+struct Term { int band, lg, kmin, npad, ntap, toff; };
 struct CorParams {
   int N, J, ext, stride, ML, n_t, TT, ntiles, taps_per_t, balloc, nbuf;
   long long rows;
@@ -345,11 +345,15 @@ struct CorParams {
   Term term[kMaxTerms];
 };
 
-template <typename T2, int Q, bool LAST>
-__device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int plane, int g, const T2* __restrict__ tp,
+// One chunk of REM taps (REM = Q except in an item's last chunk).  Step kk: every output
+// j consumes slot (j + kk) % Q; afterwards slot kk is refilled with the value Q taps
+// ahead.  In the last chunk only the refills consumed within the chunk (kk <= REM - 2)
+// are issued.
+template <int Q, int REM, bool LAST>
+__device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int plane, int g, const float2* __restrict__ tp,
                                              float (&wr)[Q], float (&wi)[Q], float (&ar)[Q], float (&ai)[Q]) {
 #pragma unroll
-  for (int kk = 0; kk < Q; ++kk) {
+  for (int kk = 0; kk < REM; ++kk) {
     const float2 t = tp[kk];
     const float nty = -t.y;
 #pragma unroll
@@ -360,7 +364,7 @@ __device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int p
       ai[j] = fmaf(t.x, wi[sl], ai[j]);
       ai[j] = fmaf(nty, wr[sl], ai[j]);
     }
-    if (!LAST || kk < Q - 1) {      // the last step's replacement is never consumed
+    if (!LAST || kk < REM - 1) {
       const float* q = pr + kk * g;
       wr[kk] = q[0];
       wi[kk] = q[plane];
@@ -368,11 +372,11 @@ __device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int p
   }
 }
 
-template <typename T2, int Q, bool LAST>
-__device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int plane, int g, const T2* __restrict__ tp,
+template <int Q, int REM, bool LAST>
+__device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int plane, int g, const int2* __restrict__ tp,
                                              unsigned (&wr)[Q], unsigned (&wi)[Q], unsigned (&ar)[Q], unsigned (&ai)[Q]) {
 #pragma unroll
-  for (int kk = 0; kk < Q; ++kk) {
+  for (int kk = 0; kk < REM; ++kk) {
     const int2 t = tp[kk];
     const unsigned tx = (unsigned)t.x, ty = (unsigned)t.y, nty = 0u - ty;
 #pragma unroll
@@ -381,12 +385,23 @@ __device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int pla
       ar[j] += tx * wr[sl] + ty * wi[sl];            // wrap-around int32 (exact mod 2^32)
       ai[j] += tx * wi[sl] + nty * wr[sl];
     }
-    if (!LAST || kk < Q - 1) {      // the last step's replacement is never consumed
+    if (!LAST || kk < REM - 1) {
       const int* q = pr + kk * g;
       wr[kk] = (unsigned)q[0];
       wi[kk] = (unsigned)q[plane];
     }
   }
+}
+
+template <bool INT, int Q, int REM>
+__device__ __forceinline__ void corr_chunk(const typename std::conditional<INT, int, float>::type* pr, int plane, int g,
+                                           const typename std::conditional<INT, int2, float2>::type* tp,
+                                           typename std::conditional<INT, unsigned, float>::type (&wr)[Q],
+                                           typename std::conditional<INT, unsigned, float>::type (&wi)[Q],
+                                           typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
+                                           typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
+  if constexpr (INT) corr_chunk_i<Q, REM, true>(pr, plane, g, tp, wr, wi, ar, ai);
+  else corr_chunk_f<Q, REM, true>(pr, plane, g, tp, wr, wi, ar, ai);
 }
 
 // One item: Q outputs q0..q0+Q-1 of residue r; band tile value for output q, tap k' at
@@ -395,7 +410,7 @@ __device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int pla
 // ragged last q-block) read at most g (Q-1) values past the tile, inside the buffer.
 template <bool INT, int Q>
 __device__ __forceinline__ void corr_item(const typename std::conditional<INT, int, float>::type* sb, int plane,
-                                          const typename std::conditional<INT, int2, float2>::type* tp, int npad,
+                                          const typename std::conditional<INT, int2, float2>::type* tp, int ntap,
                                           int r, int lg, int q0,
                                           typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
                                           typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
@@ -411,17 +426,26 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
     ai[m] = A(0);
   }
   const auto* pr = base + (Q << lg);
-  int kc = 0;
-  for (; kc + Q < npad; kc += Q, pr += Q * g) {
-    if constexpr (INT) corr_chunk_i<int2, Q, false>(pr, plane, g, tp + kc, wr, wi, ar, ai);
-    else corr_chunk_f<float2, Q, false>(pr, plane, g, tp + kc, wr, wi, ar, ai);
+  const int nfull = (ntap - 1) / Q;          // full chunks; the last chunk has 1..Q taps
+  for (int c = 0; c < nfull; ++c, pr += Q * g, tp += Q) {
+    if constexpr (INT) corr_chunk_i<Q, Q, false>(pr, plane, g, tp, wr, wi, ar, ai);
+    else corr_chunk_f<Q, Q, false>(pr, plane, g, tp, wr, wi, ar, ai);
   }
-  if constexpr (INT) corr_chunk_i<int2, Q, true>(pr, plane, g, tp + kc, wr, wi, ar, ai);
-  else corr_chunk_f<float2, Q, true>(pr, plane, g, tp + kc, wr, wi, ar, ai);
+  switch (ntap - nfull * Q) {
+    case 1: corr_chunk<INT, Q, 1>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    case 2: corr_chunk<INT, Q, 2>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    case 3: corr_chunk<INT, Q, 3>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    case 4: corr_chunk<INT, Q, 4>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    case 5: corr_chunk<INT, Q, 5>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    case 6: corr_chunk<INT, Q, 6>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    case 7: corr_chunk<INT, Q, 7>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    case 8: corr_chunk<INT, Q, 8>(pr, plane, g, tp, wr, wi, ar, ai); break;
+    default: corr_chunk<INT, Q, Q>(pr, plane, g, tp, wr, wi, ar, ai); break;
+  }
 }
 
-template <bool INT, int Q>
-__global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
+template <bool INT, int Q, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
                                                    void* __restrict__ corr, void* __restrict__ partials, CorParams p) {
   typedef typename std::conditional<INT, int, float>::type T;
   typedef typename std::conditional<INT, int2, float2>::type T2;
@@ -449,7 +473,7 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
   auto issue = [&](int step, int b) {
     const Term tm = p.term[p.J - step];
     const int g = 1 << tm.lg;
-    const int blen = TT + g * (tm.npad - 1);
+    const int blen = TT + g * (tm.ntap - 1);
     const int a = tau0 + g * tm.kmin + p.ML;
     const int a4 = a & ~3;
     const uint32_t bytes = (uint32_t)(((a - a4) + blen + 3) & ~3) * 4u;
@@ -486,7 +510,7 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
       sb += (a & 3);
     } else {
       // periodic: wrapped positions, batched cooperative loads (8 in flight per thread)
-      const int blen = TT + g * (tm.npad - 1);
+      const int blen = TT + g * (tm.ntap - 1);
       const int pos0 = tau0 + g * tm.kmin;
       const T* pre = brow + (size_t)tm.band * 2 * p.stride;
       for (int x0 = threadIdx.x; x0 < blen; x0 += 8 * blockDim.x) {
@@ -515,7 +539,7 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
       const int r = w & (g - 1);
       const int q0 = (w >> tm.lg) * Q;
       A ar[Q], ai[Q];
-      corr_item<INT, Q>(sb, plane, stap + tm.toff, tm.npad, r, tm.lg, q0, ar, ai);
+      corr_item<INT, Q>(sb, plane, stap + tm.toff, tm.ntap, r, tm.lg, q0, ar, ai);
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
         if (q0 + j < nq) {
@@ -529,23 +553,48 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
     __syncthreads();
     if (tma && !dbl && threadIdx.x == 0 && step < p.J) issue(step + 1, 0);
     cur ^= 1;
-    // store corr_ti and reduce the peak partial of this tile
+    // store corr_ti (4 lags per thread-iteration, 2 x 16-byte stores) and reduce this tile's
+    // peak partial: lags increase within a thread, so a strict '>' keeps the smallest lag.
     const T* a = acc + (size_t)cur * 2 * TT;
     T2* dst = p.want_corr ? static_cast<T2*>(corr) + (((size_t)row * p.n_t + t) * (p.J + 1) + ti) * p.N + tau0 : nullptr;
     PK best;
-    best.m2 = 0; best.tau = 0x7fffffff; best.re = 0; best.im = 0;
-    for (int tl = threadIdx.x; tl < TT; tl += blockDim.x) {
-      T2 v;
-      v.x = a[tl]; v.y = a[TT + tl];
-      if (dst) dst[tl] = v;
-      if (p.want_peaks) {
-        if constexpr (INT) {
-          const unsigned long long m = mag2i(v.x, v.y);
-          if (best.tau == 0x7fffffff || beats(m, tau0 + tl, best.m2, best.tau)) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
-        } else {
-          const float m = mag2f(v.x, v.y);
-          if (best.tau == 0x7fffffff || beats(m, tau0 + tl, best.m2, best.tau)) { best.m2 = m; best.tau = tau0 + tl; best.re = v.x; best.im = v.y; }
+    best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0;
+    auto consider = [&](T re, T im, int tau) {
+      if constexpr (INT) {
+        const unsigned long long m = mag2i(re, im);
+        const bool bt = (best.tau < 0) || (m > best.m2);
+        best.m2 = bt ? m : best.m2; best.tau = bt ? tau : best.tau; best.re = bt ? re : best.re; best.im = bt ? im : best.im;
+      } else {
+        const float m = mag2f(re, im);
+        const bool bt = (best.tau < 0) || (m > best.m2);
+        best.m2 = bt ? m : best.m2; best.tau = bt ? tau : best.tau; best.re = bt ? re : best.re; best.im = bt ? im : best.im;
+      }
+    };
+    if ((TT & 3) == 0) {
+      for (int tl = threadIdx.x * 4; tl < TT; tl += blockDim.x * 4) {
+        typedef typename std::conditional<INT, int4, float4>::type T4;
+        const T4 vr = *reinterpret_cast<const T4*>(a + tl);
+        const T4 vi = *reinterpret_cast<const T4*>(a + TT + tl);
+        if (dst) {
+          T4 o0, o1;
+          o0.x = vr.x; o0.y = vi.x; o0.z = vr.y; o0.w = vi.y;
+          o1.x = vr.z; o1.y = vi.z; o1.z = vr.w; o1.w = vi.w;
+          *reinterpret_cast<T4*>(dst + tl) = o0;
+          *reinterpret_cast<T4*>(dst + tl + 2) = o1;
         }
+        if (p.want_peaks) {
+          consider(vr.x, vi.x, tau0 + tl);
+          consider(vr.y, vi.y, tau0 + tl + 1);
+          consider(vr.z, vi.z, tau0 + tl + 2);
+          consider(vr.w, vi.w, tau0 + tl + 3);
+        }
+      }
+    } else {
+      for (int tl = threadIdx.x; tl < TT; tl += blockDim.x) {
+        T2 v;
+        v.x = a[tl]; v.y = a[TT + tl];
+        if (dst) dst[tl] = v;
+        if (p.want_peaks) consider(v.x, v.y, tau0 + tl);
       }
     }
     if (p.want_peaks) {
@@ -556,7 +605,7 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
         o.tau = __shfl_down_sync(0xffffffffu, best.tau, off);
         o.re = __shfl_down_sync(0xffffffffu, best.re, off);
         o.im = __shfl_down_sync(0xffffffffu, best.im, off);
-        if (o.tau != 0x7fffffff && (best.tau == 0x7fffffff || beats(o.m2, o.tau, best.m2, best.tau))) best = o;
+        if (o.tau >= 0 && (best.tau < 0 || beats(o.m2, o.tau, best.m2, best.tau))) best = o;
       }
       if ((threadIdx.x & 31) == 0) red[ti][threadIdx.x >> 5] = best;
     }
@@ -567,7 +616,7 @@ __global__ void __launch_bounds__(256) k_correlate(const void* __restrict__ band
       PK b = red[ti][0];
       for (int w = 1; w < kWarps; ++w) {
         const PK o = red[ti][w];
-        if (o.tau != 0x7fffffff && (b.tau == 0x7fffffff || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
+        if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
       }
       static_cast<PK*>(partials)[(((size_t)row * p.n_t + t) * (p.J + 1) + ti) * p.ntiles + tile] = b;
     }

@@ -133,13 +133,12 @@ static void configure(sidwt_plan_s* p) {
     off += p->npad[i];
   }
   p->taps_per_t = off;
-  // correlation reach -> band margins (DESIGN.md R-D6 GPU).  The right margin covers the
-  // Q-padded tap range too, so every band value K2 touches exists (no clamps).
+  // correlation reach -> band margins (DESIGN.md R-D6 GPU): every band value K2 reads exists.
   int ML = 0, MR = 0;
   for (int i = 0; i <= J; ++i) {
     const int g = 1 << (i < J ? i + 1 : J);
     ML = std::max(ML, -g * p->kmin[i]);
-    MR = std::max(MR, g * (p->kmin[i] + p->npad[i] - 1));
+    MR = std::max(MR, g * (p->kmin[i] + p->cnt[i] - 1));
   }
   if (p->ext == SIDWT_EXT_PERIODIC) { ML = 0; MR = 0; }
   p->ML = ML; p->MR = MR;
@@ -181,8 +180,8 @@ static void configure(sidwt_plan_s* p) {
   for (int i = 0; i <= J; ++i) {
     const int lg = i < J ? i + 1 : J;
     c.term[i].band = i; c.term[i].lg = lg; c.term[i].kmin = p->kmin[i];
-    c.term[i].npad = p->npad[i]; c.term[i].toff = p->toff[i];
-    blen_max = std::max<int>(blen_max, (int)TT + (1 << lg) * (p->npad[i] - 1 + kQ - 1));
+    c.term[i].npad = p->npad[i]; c.term[i].ntap = p->cnt[i]; c.term[i].toff = p->toff[i];
+    blen_max = std::max<int>(blen_max, (int)TT + (1 << lg) * (p->cnt[i] - 1 + kQ - 1));
   }
   c.balloc = (int)rup(blen_max + 4, 4);          // + alignment shift of the bulk copy
   // double-buffered band tiles when they fit (prefetch overlaps compute), else single
@@ -310,20 +309,17 @@ static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t
   const int64_t grid = rows * p->n_t * c.ntiles;
   if (grid > 0x7fffffffLL) return SIDWT_ERR_RANGE;
   cudaError_t e;
-  if (is_int(p)) {
-    auto kern = k_correlate<true, kQ>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cor_smem);
-    if (e == cudaSuccess) {
-      kern<<<(unsigned)grid, kK2Threads, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
-      e = cudaGetLastError();
-    }
-  } else {
-    auto kern = k_correlate<false, kQ>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cor_smem);
-    if (e == cudaSuccess) {
-      kern<<<(unsigned)grid, kK2Threads, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
-      e = cudaGetLastError();
-    }
+  int minb = 3;                       // 3 CTAs x 8 warps per SM (measured best on C2)
+  if (const char* ev = std::getenv("SIDWT_K2_MINB")) minb = std::max(1, std::min(4, atoi(ev)));
+  void (*kern)(const void*, const void*, void*, void*, CorParams);
+  if (is_int(p)) kern = minb <= 1 ? k_correlate<true, kQ, 1> : minb == 2 ? k_correlate<true, kQ, 2>
+                      : minb == 3 ? k_correlate<true, kQ, 3> : k_correlate<true, kQ, 4>;
+  else kern = minb <= 1 ? k_correlate<false, kQ, 1> : minb == 2 ? k_correlate<false, kQ, 2>
+              : minb == 3 ? k_correlate<false, kQ, 3> : k_correlate<false, kQ, 4>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cor_smem);
+  if (e == cudaSuccess) {
+    kern<<<(unsigned)grid, kK2Threads, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
+    e = cudaGetLastError();
   }
   p->last_launches = 1;
   if (e == cudaSuccess && peaks) {
