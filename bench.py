@@ -227,9 +227,11 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    from paper_cs_0607001_b200 import dist as D
     R = args.rows or cfg.rows
     tm = W.templates(cfg)
-    rows_h = W.make_rows(cfg, rank * R, R, tm)          # weak scaling: each rank its own batch
+    r0, R = D.weak_rows(rank, R)                        # weak scaling: each rank its own batch
+    rows_h = W.make_rows(cfg, r0, R, tm)
     plan = Plan(cfg.family, cfg.levels, cfg.N, R, cfg.ext, device=dev).load_templates(tm)
     stream = torch.cuda.current_stream(dev)
     d_rows = plan.rows_to_device(rows_h)
@@ -275,11 +277,7 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = t0.elapsed_time(t1) / args.steps
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = D.max_over_ranks(t0.elapsed_time(t1) / args.steps, device=dev)
     value = world * R * cfg.N / (ms * 1e-3)
 
     # e2e: host rows (pinned) -> device -> path -> lag/val back to host, through the C ABI
@@ -303,11 +301,7 @@ def main():
             plan.execute_host(h_rows, R, h_lag, h_val, stream)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / args.steps
-        if world > 1:
-            tt = torch.tensor([ems], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+        ems = D.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=dev)
         assert np.array_equal(h_lag.numpy(), lag.cpu().numpy()), "e2e lags differ from the device path"
         e2e = {"value": world * R * cfg.N / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": R * cfg.N * sb,
