@@ -160,28 +160,84 @@ __global__ void k_template_pyramid(const void* __restrict__ x, void* __restrict_
 // ---------------------------------------------------------------------------
 // K1: fused multi-level SIDWT lifting of one (row, component, tile).
 //
-// smem: U[lbuf] (in-place working band, fine-grid positions A .. A+lbuf) and
-// Wst[tile_len] (detail staging).  Level s (stride h = 2^{s-1}): thread w owns a
-// run of RV consecutive pairs j0..j0+RV-1 of branch rho = w mod h (fine-grid
-// positions rho + h j), loads RV + HL + HR values, lifts in registers, then
-// (after a barrier) writes U_s in place and W_s into staging; one thread stores
-// the staging plane with a bulk async copy (TMA engine) while the next level
-// computes.  Each input sample is read from HBM once per component; every band
-// byte is written once.  Bank-conflict free: RV odd.
+// smem: U[padl + lbuf + padr] (in-place working band, fine-grid positions
+// A .. A+lbuf at U[padl ..]) and Wst[lbuf + padr] (detail staging, same
+// indexing).  Level s (stride h = 2^{s-1}): thread w owns a run of RV
+// consecutive pairs j0..j0+RV-1 of branch rho = w mod h (fine-grid positions
+// rho + h j), loads RV + HL + HR values, lifts in registers, then (after a
+// barrier) writes U_s in place and W_s into staging; one thread stores the
+// staging plane with a bulk async copy (TMA engine) while the next level
+// computes.  The level stride is a compile-time constant (one instantiation per
+// level) so every shared-memory access is one instruction with an immediate
+// offset; the zeroed pads absorb the reads and writes that run past the buffer
+// ends, so there are no index clamps or store predicates: positions whose value
+// depends on the pads lie inside the halo, which is never stored.  Each input
+// sample is read from HBM once per component; every band byte is written once.
+// Bank-conflict free: RV odd.
 // ---------------------------------------------------------------------------
 struct AnaParams {
   int N, J, ext, stride, ML;
   int tile_len, ntiles, halo_l, lbuf;
+  int padl, padr;
   long long rows;
 };
+
+template <int FAM, int RV, int LH>
+__device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict__ U, typename Dual<FAM>::T* __restrict__ Wst,
+                                              int lbuf) {
+  typedef typename Dual<FAM>::T T;
+  constexpr int HL = Dual<FAM>::HL, HR = Dual<FAM>::HR, WIN = RV + HL + HR;
+  constexpr int h = 1 << LH;
+  const int w = threadIdx.x;
+  const int rho = w & (h - 1);
+  const int j0 = (w >> LH) * RV;
+  const int len = (lbuf - rho + h - 1) >> LH;     // positions rho + h j < lbuf
+  const bool active = j0 < len;
+  const int u0 = rho + (j0 << LH);
+  T c[RV], d[RV];
+  if (active) {
+    const T* src = U + u0 - HL * h;
+    T v[WIN];
+#pragma unroll
+    for (int i = 0; i < WIN; ++i) v[i] = src[i * h];
+    Dual<FAM>::template run<RV>(v, c, d);
+  }
+  if (threadIdx.x == 0 && LH > 0) bulk_wait_read_all();   // staging free again
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < RV; ++i) {
+      U[u0 + i * h] = c[i];
+      Wst[u0 + i * h] = d[i];
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+}
+
+// Levels LH = 0 .. J-1 as straight-line code (compile-time stride per level), each
+// followed by the bulk store of its detail plane.
+template <int FAM, int RV, int LH>
+__device__ __forceinline__ void analyze_levels(int J, typename Dual<FAM>::T* U, typename Dual<FAM>::T* Wst, int lbuf,
+                                               typename Dual<FAM>::T* plane0, size_t band_step, int halo_l, int out_len) {
+  if constexpr (LH < 16) {
+    if (LH >= J) return;
+    analyze_level<FAM, RV, LH>(U, Wst, lbuf);
+    if (threadIdx.x == 0) {
+      bulk_store_s2g(plane0 + (size_t)LH * band_step, Wst + halo_l, (uint32_t)(out_len * sizeof(typename Dual<FAM>::T)));
+      bulk_commit();
+    }
+    analyze_levels<FAM, RV, LH + 1>(J, U, Wst, lbuf, plane0, band_step, halo_l, out_len);
+  }
+}
 
 template <int FAM, int RV>
 __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_in, void* __restrict__ bands, AnaParams p) {
   typedef typename Dual<FAM>::T T;
-  constexpr int HL = Dual<FAM>::HL, HR = Dual<FAM>::HR, WIN = RV + HL + HR;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* U = reinterpret_cast<T*>(smem_raw);
-  T* Wst = U + p.lbuf;
+  T* Ubuf = reinterpret_cast<T*>(smem_raw);
+  T* U = Ubuf + p.padl;
+  T* Wst = Ubuf + p.padl + p.lbuf + p.padr;
 
   const int tile = blockIdx.x % p.ntiles;
   const long long rc = blockIdx.x / p.ntiles;
@@ -191,6 +247,9 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
   const int out_len = min(p.tile_len, p.stride - tstart);
   const long long A = (long long)(-p.ML + tstart) - p.halo_l;
 
+  // zero the pads (reads past the buffer ends see finite values)
+  for (int u = threadIdx.x; u < p.padl; u += blockDim.x) Ubuf[u] = T(0);
+  for (int u = threadIdx.x; u < p.padr; u += blockDim.x) U[p.lbuf + u] = T(0);
   // load the extended row segment (one component); 8 independent loads in flight per thread
   {
     const int N = p.N;
@@ -243,46 +302,7 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
   T* plane0 = static_cast<T*>(bands) + ((size_t)row * (p.J + 1) * 2 + comp) * p.stride + tstart;
   const size_t band_step = (size_t)2 * p.stride;
 
-  for (int s = 1; s <= p.J; ++s) {
-    const int lh = s - 1;
-    const int h = 1 << lh;
-    const int w = threadIdx.x;
-    const int rho = w & (h - 1);
-    const int j0 = (w >> lh) * RV;
-    const int len = (p.lbuf - rho + h - 1) >> lh;   // positions rho + h j < lbuf
-    const bool active = j0 < len;
-    T c[RV], d[RV];
-    if (active) {
-      T v[WIN];
-#pragma unroll
-      for (int i = 0; i < WIN; ++i) {
-        int j = j0 - HL + i;
-        j = max(0, min(j, len - 1));
-        v[i] = U[rho + (j << lh)];
-      }
-      Dual<FAM>::template run<RV>(v, c, d);
-    }
-    if (threadIdx.x == 0 && s > 1) bulk_wait_read_all();   // staging free again
-    __syncthreads();
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < RV; ++i) {
-        const int j = j0 + i;
-        if (j < len) {
-          const int u = rho + (j << lh);
-          U[u] = c[i];
-          const int wu = u - p.halo_l;
-          if (wu >= 0 && wu < out_len) Wst[wu] = d[i];
-        }
-      }
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      bulk_store_s2g(plane0 + (size_t)(s - 1) * band_step, Wst, (uint32_t)(out_len * sizeof(T)));
-      bulk_commit();
-    }
-  }
+  analyze_levels<FAM, RV, 0>(p.J, U, Wst, p.lbuf, plane0, band_step, p.halo_l, out_len);
   if (threadIdx.x == 0) {
     bulk_store_s2g(plane0 + (size_t)p.J * band_step, U + p.halo_l, (uint32_t)(out_len * sizeof(T)));
     bulk_commit();

@@ -166,8 +166,15 @@ static void configure(sidwt_plan_s* p) {
   ntiles = cdiv(p->stride, tile_len);
   p->ana.N = (int)p->N; p->ana.J = J; p->ana.ext = p->ext; p->ana.stride = (int)p->stride; p->ana.ML = ML;
   p->ana.tile_len = (int)tile_len; p->ana.ntiles = (int)ntiles; p->ana.halo_l = (int)halo_l; p->ana.lbuf = (int)lbuf;
+  // pads absorbing the clamp-free window reads / run writes past the buffer ends (top level)
+  int HL = 1, HR = 3;
+  if (p->fam == F97) { HL = Dual<F97>::HL; HR = Dual<F97>::HR; }
+  else if (p->fam == FD4) { HL = Dual<FD4>::HL; HR = Dual<FD4>::HR; }
+  const int64_t htop = 1LL << (J - 1);
+  p->ana.padl = (int)rup(HL * htop, 4);
+  p->ana.padr = (int)rup((kRV - 1 + HR) * htop, 4);
   p->ana_threads = (int)std::min<int64_t>(512, rup(threads, 32));
-  p->ana_smem = (size_t)(lbuf + tile_len) * 4;
+  p->ana_smem = (size_t)(p->ana.padl + 2 * (lbuf + p->ana.padr)) * 4;
 
   // ---- K2 tiling
   int64_t tt_target = 2048;
