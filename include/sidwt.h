@@ -116,7 +116,13 @@ sidwt_status sidwt_analyze(sidwt_plan plan, const void* d_rows, int64_t rows, vo
 /* Correlate bands against every loaded template at every scale and lag.
  * d_corr: device, [rows][n_templates][levels+1][N] complex64 (int32x2 for the
  *         integer family: the exact integer correlation reduced mod 2^32).
- *         Scale index s = 0 (finest, = textbook correlation) .. levels (U_J only). */
+ *         Scale index s = 0 (finest, = textbook correlation) .. levels (U_J only).
+ * Template banks (float families, n_templates >= 16, N a multiple of 512) form a
+ * dense contraction and run on the tensor cores (tcgen05.mma): fp32 operands split
+ * into bf16 hi + lo, three products (hi.hi + hi.lo + lo.hi) accumulated in fp32;
+ * error ~1e-5 of the peak |corr| (the fp32 SIMT kernel: ~1e-7).  Environment
+ * SIDWT_TC=0 disables this path, SIDWT_TC=1 forces it for any bank size; read at
+ * template_load.  Otherwise the per-lag FP32 (INT32) SIMT kernel runs. */
 sidwt_status sidwt_correlate(sidwt_plan plan, const void* d_bands, int64_t rows, void* d_corr,
                              void* stream);
 
@@ -155,6 +161,10 @@ int64_t sidwt_corr_bytes(sidwt_plan plan, int64_t rows);
  * taps as float2 (int2 for the integer family), unconjugated.  host_taps may
  * be NULL to query only.  Returns the number of taps per template or -1. */
 int64_t sidwt_template_taps(sidwt_plan plan, void* host_taps, int32_t* kmin, int32_t* count);
+
+/* 1 if sidwt_correlate* of this plan run on the tensor cores (bank path), 0 if on the
+ * SIMT pipes, -1 before template_load. */
+int sidwt_uses_tensor_cores(sidwt_plan plan);
 
 /* Number of kernel launches the last analyze / correlate / peaks / correlate_peaks
  * call enqueued (for launch accounting). */

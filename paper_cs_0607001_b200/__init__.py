@@ -139,5 +139,8 @@ class Plan:
     def execute_host(self, h_rows, rows: int, h_lag, h_val=None, stream=None):
         _native.sidwt_execute_host(self.handle, h_rows, rows, h_lag, h_val, self._stream(stream))
 
+    def uses_tensor_cores(self) -> bool:
+        return _native.sidwt_uses_tensor_cores(self.handle) == 1
+
     def last_launches(self) -> int:
         return _native.sidwt_last_launches(self.handle)

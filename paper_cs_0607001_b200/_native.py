@@ -13,7 +13,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libsidwt.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sidwt.cu", "kernels.cuh", "lifting.cuh")] + [
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sidwt.cu", "kernels.cuh", "lifting.cuh", "corr_tc.cuh")] + [
     os.path.join(ROOT, "include", "sidwt.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -30,7 +30,7 @@ STATUS = {0: "SIDWT_OK", 1: "SIDWT_ERR_PARAM", 2: "SIDWT_ERR_LENGTH", 3: "SIDWT_
 EXPORTS = ["sidwt_plan_create", "sidwt_plan_destroy", "sidwt_template_load", "sidwt_analyze",
            "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_execute_host",
            "sidwt_band_stride", "sidwt_band_offset", "sidwt_bands_bytes", "sidwt_corr_bytes",
-           "sidwt_template_taps", "sidwt_last_launches", "sidwt_status_string"]
+           "sidwt_template_taps", "sidwt_last_launches", "sidwt_uses_tensor_cores", "sidwt_status_string"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -79,6 +79,8 @@ def lib():
         L.sidwt_template_taps.restype = I64
         L.sidwt_last_launches.argtypes = [P]
         L.sidwt_last_launches.restype = I
+        L.sidwt_uses_tensor_cores.argtypes = [P]
+        L.sidwt_uses_tensor_cores.restype = I
         L.sidwt_status_string.argtypes = [I]
         L.sidwt_status_string.restype = C.c_char_p
         _lib = L
@@ -171,6 +173,10 @@ def sidwt_template_taps(plan, host_taps=None, kmin=None, count=None) -> int:
 
 def sidwt_last_launches(plan) -> int:
     return lib().sidwt_last_launches(plan)
+
+
+def sidwt_uses_tensor_cores(plan) -> int:
+    return lib().sidwt_uses_tensor_cores(plan)
 
 
 def sidwt_status_string(st: int) -> str:

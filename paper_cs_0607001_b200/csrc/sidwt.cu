@@ -12,6 +12,7 @@
 
 #include "../../include/sidwt.h"
 #include "kernels.cuh"
+#include "corr_tc.cuh"
 
 using namespace sidwt;
 
@@ -49,6 +50,11 @@ struct sidwt_plan_s {
   size_t partials_bytes = 0;
   void *w_rows = nullptr, *w_bands = nullptr, *w_corr = nullptr, *w_lag = nullptr, *w_val = nullptr;
   int last_launches = 0;
+  // tensor-core bank path (corr_tc.cuh)
+  bool tc = false;
+  TcParams tcp{};
+  void* d_img = nullptr;
+  size_t tc_smem = 0;
 };
 
 static bool is_int(const sidwt_plan_s* p) { return p->fam == SIDWT_LEGALL53_INT; }
@@ -87,7 +93,7 @@ sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t 
 }
 
 static void free_ws(sidwt_plan_s* p) {
-  void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val};
+  void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val, &p->d_img};
   for (void** b : bufs) { if (*b) cudaFree(*b); *b = nullptr; }
   p->partials_bytes = 0;
 }
@@ -110,6 +116,7 @@ int64_t sidwt_corr_bytes(sidwt_plan p, int64_t rows) {
   return rows * p->n_t * (p->J + 1) * p->N * 8;
 }
 int sidwt_last_launches(sidwt_plan p) { return p ? p->last_launches : 0; }
+int sidwt_uses_tensor_cores(sidwt_plan p) { return (p && p->loaded) ? (p->tc ? 1 : 0) : -1; }
 
 // ---------------------------------------------------------------------------
 // Template load: supports, margins, tiling, and the device pyramid (K0).
@@ -198,6 +205,41 @@ static void configure(sidwt_plan_s* p) {
   p->cor_smem = smem(c.nbuf);
 }
 
+// Tensor-core bank path: float families, N a multiple of the 512-lag CTA tile, a
+// template bank (n_t >= 16; SIDWT_TC=0 disables, SIDWT_TC=1 forces it for any n_t).
+static void configure_tc(sidwt_plan_s* p) {
+  p->tc = false;
+  if (is_int(p) || p->N % kTcLags != 0) return;
+  const char* env = std::getenv("SIDWT_TC");
+  if (env && env[0] == '0') return;
+  if (p->n_t < 16 && !(env && env[0] == '1')) return;
+  TcParams& t = p->tcp;
+  t = TcParams{};
+  t.N = (int)p->N; t.J = p->J; t.ext = p->ext; t.stride = (int)p->stride; t.ML = p->ML; t.n_t = p->n_t;
+  t.n_mt = (int)cdiv(p->n_t, kTcTemplates);
+  t.ntiles = (int)(p->N / kTcLags);
+  int kofs = 0, nz_max = 0;
+  for (int step = 0; step <= p->J; ++step) {
+    const int ti = p->J - step;
+    TcTerm& m = t.term[step];
+    const int lg = ti < p->J ? ti + 1 : p->J;
+    m.band = ti; m.g = 1 << lg; m.ge = std::min(m.g, 8); m.f = m.g / m.ge;
+    m.kmin = p->kmin[ti]; m.ntap = p->cnt[ti]; m.toff = p->toff[ti];
+    const int ntap_e = (m.ntap - 1) * m.f + 1;
+    m.kp = (int)rup(ntap_e, 16);
+    m.ksteps = 2 * m.kp / 16;
+    m.kofs = kofs;
+    kofs += m.ksteps;
+    m.nz = (kTcLags - 8) / m.ge + m.kp;
+    nz_max = std::max(nz_max, m.nz);
+  }
+  t.total_ksteps = kofs;
+  t.nz_max = (int)rup(nz_max, 8);
+  p->tc_smem = 1024 + (size_t)kTcStages * 8192 + (size_t)4 * t.nz_max * 16 + (size_t)2 * kTcTemplates * sizeof(PeakF);
+  if (p->tc_smem > 227 * 1024) return;
+  p->tc = true;
+}
+
 static sidwt_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return SIDWT_OK;
   if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); return SIDWT_ERR_OOM; }
@@ -211,6 +253,7 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   if (n_templates < 1 || n_templates > 65536) return SIDWT_ERR_DIMENSION;
   if (p->d_taps) { cudaFree(p->d_taps); p->d_taps = nullptr; }
   if (p->d_partials) { cudaFree(p->d_partials); p->d_partials = nullptr; p->partials_bytes = 0; }
+  if (p->d_img) { cudaFree(p->d_img); p->d_img = nullptr; }
   p->loaded = false;
   p->T = (int)T; p->n_t = n_templates;
   configure(p);
@@ -240,6 +283,23 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   if (e != cudaSuccess) {
     if (p->d_taps) { cudaFree(p->d_taps); p->d_taps = nullptr; }
     return cuda_status(e);
+  }
+  configure_tc(p);
+  if (p->tc) {
+    const size_t img_bytes = (size_t)p->tcp.n_mt * p->tcp.total_ksteps * 8192;
+    e = cudaMalloc(&p->d_img, img_bytes);
+    if (e == cudaSuccess) {
+      const long long items = (long long)p->tcp.n_mt * p->tcp.total_ksteps * 2 * kTcM;
+      k_tc_images<<<(unsigned)cdiv(items, 256), 256>>>(static_cast<const float2*>(p->d_taps), p->taps_per_t, p->tcp,
+                                                        static_cast<unsigned char*>(p->d_img));
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      if (p->d_img) { cudaFree(p->d_img); p->d_img = nullptr; }
+      cudaFree(p->d_taps); p->d_taps = nullptr;
+      return cuda_status(e);
+    }
   }
   p->loaded = true;
   return SIDWT_OK;
@@ -296,7 +356,7 @@ sidwt_status sidwt_analyze(sidwt_plan p, const void* d_rows, int64_t rows, void*
 
 static sidwt_status ensure_partials(sidwt_plan_s* p) {
   const size_t rec = is_int(p) ? sizeof(PeakI) : sizeof(PeakF);
-  const size_t need = (size_t)p->batch * p->n_t * (p->J + 1) * p->cor.ntiles * rec;
+  const size_t need = (size_t)p->batch * p->n_t * (p->J + 1) * (p->tc ? p->tcp.ntiles : p->cor.ntiles) * rec;
   if (p->partials_bytes >= need) return SIDWT_OK;
   if (p->d_partials) cudaFree(p->d_partials);
   p->d_partials = nullptr;
@@ -307,8 +367,36 @@ static sidwt_status ensure_partials(sidwt_plan_s* p) {
   return SIDWT_OK;
 }
 
+static sidwt_status correlate_tc(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
+                                 int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
+  TcParams t = p->tcp;
+  t.rows = rows;
+  t.want_corr = d_corr != nullptr;
+  t.want_peaks = peaks;
+  const int64_t grid = rows * t.n_mt * t.ntiles;
+  if (grid > 0x7fffffffLL) return SIDWT_ERR_RANGE;
+  auto kern = k_correlate_tc<kTcStages>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tc_smem);
+  if (e == cudaSuccess) {
+    kern<<<(unsigned)grid, kTcThreads, p->tc_smem, s>>>(static_cast<const float*>(d_bands),
+                                                        static_cast<const unsigned char*>(p->d_img),
+                                                        static_cast<float2*>(d_corr),
+                                                        static_cast<PeakF*>(p->d_partials), t);
+    e = cudaGetLastError();
+  }
+  p->last_launches = 1;
+  if (e == cudaSuccess && peaks) {
+    const int64_t count = rows * p->n_t * (p->J + 1);
+    k_peaks_finalize<false><<<(unsigned)cdiv(count, 256), 256, 0, s>>>(p->d_partials, t.ntiles, count, d_lag, d_val);
+    e = cudaGetLastError();
+    p->last_launches = 2;
+  }
+  return cuda_status(e);
+}
+
 static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
                                    int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
+  if (p->tc) return correlate_tc(p, d_bands, rows, d_corr, d_lag, d_val, peaks, s);
   CorParams c = p->cor;
   c.rows = rows;
   c.want_corr = d_corr != nullptr;
