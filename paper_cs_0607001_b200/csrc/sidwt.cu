@@ -52,6 +52,7 @@ struct sidwt_plan_s {
   int last_launches = 0;
   // tensor-core bank path (corr_tc.cuh)
   bool tc = false;
+  int tc_sms = 148;
   TcParams tcp{};
   void* d_img = nullptr;
   size_t tc_smem = 0;
@@ -205,11 +206,11 @@ static void configure(sidwt_plan_s* p) {
   p->cor_smem = smem(c.nbuf);
 }
 
-// Tensor-core bank path: float families, N a multiple of the 512-lag CTA tile, a
+// Tensor-core bank path: float families, N a multiple of the 512-lag tile pair, a
 // template bank (n_t >= 16; SIDWT_TC=0 disables, SIDWT_TC=1 forces it for any n_t).
 static void configure_tc(sidwt_plan_s* p) {
   p->tc = false;
-  if (is_int(p) || p->N % kTcLags != 0) return;
+  if (is_int(p) || p->N % kTcTilePair != 0) return;
   const char* env = std::getenv("SIDWT_TC");
   if (env && env[0] == '0') return;
   if (p->n_t < 16 && !(env && env[0] == '1')) return;
@@ -217,8 +218,8 @@ static void configure_tc(sidwt_plan_s* p) {
   t = TcParams{};
   t.N = (int)p->N; t.J = p->J; t.ext = p->ext; t.stride = (int)p->stride; t.ML = p->ML; t.n_t = p->n_t;
   t.n_mt = (int)cdiv(p->n_t, kTcTemplates);
-  t.ntiles = (int)(p->N / kTcLags);
-  int kofs = 0, nz_max = 0;
+  t.ntiles = (int)(p->N / 256);
+  int kofs = 0, nz_max = 0, kmax = 0, lmax = 0;
   for (int step = 0; step <= p->J; ++step) {
     const int ti = p->J - step;
     TcTerm& m = t.term[step];
@@ -230,13 +231,28 @@ static void configure_tc(sidwt_plan_s* p) {
     m.ksteps = 2 * m.kp / 16;
     m.kofs = kofs;
     kofs += m.ksteps;
-    m.nz = (kTcLags - 8) / m.ge + m.kp;
+    m.nz = (256 - 8) / m.ge + m.kp;
     nz_max = std::max(nz_max, m.nz);
+    kmax = std::max(kmax, m.ksteps);
+    lmax = std::max(lmax, m.ge * (m.nz - 1) + 8);
   }
   t.total_ksteps = kofs;
   t.nz_max = (int)rup(nz_max, 8);
-  p->tc_smem = 1024 + (size_t)kTcStages * 8192 + (size_t)4 * t.nz_max * 16 + (size_t)2 * kTcTemplates * sizeof(PeakF);
-  if (p->tc_smem > 227 * 1024) return;
+  t.stg_len = (int)rup(lmax + 8, 8);
+  t.npairs = 0;
+  t.stages = 0;
+  const TcSmem base = tc_smem_layout(t);                  // with 0 stages
+  const int budget = 227 * 1024;
+  const int fit = (budget - base.total) / 8192;
+  if (fit < 4) return;
+  t.stages = std::min(kTcMaxStages, fit);
+  t.a_shared = t.stages >= kmax ? 1 : 0;
+  if (const char* e = std::getenv("SIDWT_TC_SHARED")) t.a_shared = (atoi(e) != 0) && t.a_shared;
+  p->tc_smem = (size_t)tc_smem_layout(t).total;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p->tc_sms = sms;
   p->tc = true;
 }
 
@@ -373,15 +389,14 @@ static sidwt_status correlate_tc(sidwt_plan_s* p, const void* d_bands, int64_t r
   t.rows = rows;
   t.want_corr = d_corr != nullptr;
   t.want_peaks = peaks;
-  const int64_t grid = rows * t.n_mt * t.ntiles;
-  if (grid > 0x7fffffffLL) return SIDWT_ERR_RANGE;
-  auto kern = k_correlate_tc<kTcStages>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tc_smem);
+  t.npairs = rows * t.n_mt * t.ntiles / 2;
+  const int64_t grid = std::min<int64_t>(t.npairs, p->tc_sms);
+  cudaError_t e = cudaFuncSetAttribute(k_correlate_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tc_smem);
   if (e == cudaSuccess) {
-    kern<<<(unsigned)grid, kTcThreads, p->tc_smem, s>>>(static_cast<const float*>(d_bands),
-                                                        static_cast<const unsigned char*>(p->d_img),
-                                                        static_cast<float2*>(d_corr),
-                                                        static_cast<PeakF*>(p->d_partials), t);
+    k_correlate_tc<<<(unsigned)grid, kTcThreads, p->tc_smem, s>>>(static_cast<const float*>(d_bands),
+                                                                  static_cast<const unsigned char*>(p->d_img),
+                                                                  static_cast<float2*>(d_corr),
+                                                                  static_cast<PeakF*>(p->d_partials), t);
     e = cudaGetLastError();
   }
   p->last_launches = 1;
