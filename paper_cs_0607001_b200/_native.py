@@ -39,6 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in SOURCES)
     if force or stale:
         cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(HERE, "csrc", "sidwt.cu")]
+        if os.environ.get("SIDWT_TC_PROFILE"):        # debug: timed role waits in the tensor-core kernel
+            cmd.insert(1, "-DSIDWT_TC_PROFILE")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)

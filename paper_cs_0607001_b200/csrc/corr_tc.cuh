@@ -27,17 +27,19 @@
 // the epilogue stores (and reduces to per-tile peak partials) before term i-1's
 // MMAs may accumulate on it.  Kernel structure: see k_correlate_tc below.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace sidwt {
 
 constexpr int kTcTilePair = 512;      // lags of a tile pair (two 256-lag accumulators)
 constexpr int kTcM = 128;             // MMA M: 64 templates x (re, im)
 constexpr int kTcTemplates = 64;
-constexpr int kTcMaxStages = 32;      // template-operand ring depth limit (8 KB per stage)
-constexpr int kTcThreads = 256;
+constexpr int kTcMaxStages = 16;      // template-operand ring depth limit
+constexpr int kTcStageBytes = 16384;  // ring stage: two K steps x (hi, lo) x 4 KB
 
 struct TcTerm {
   int band, g, ge, f, kmin, ntap;     // f = g / ge (zero-stuffing factor)
@@ -49,6 +51,7 @@ struct TcTerm {
 };
 
 struct TcParams {
+  CUtensorMap tmap;                   // corr as a 4-D tensor [rows][n_t][J+1][N] of 8-byte elements
   int N, J, ext, stride, ML, n_t, n_mt, ntiles, total_ksteps, nz_max;   // ntiles: 256-lag tiles per row
   int want_corr, want_peaks;
   long long rows;
@@ -56,6 +59,7 @@ struct TcParams {
   int a_shared;                       // 1: every template K step feeds both units of a tile pair
   int stg_len;                        // band staging floats per plane
   long long npairs;                   // rows * n_mt * ntiles / 2
+  int prof;                           // debug: CTA 0 prints per-role wait cycles (SIDWT_TC_PROF=1)
   TcTerm term[17];                    // indexed by processing step (0 = coarsest, A_J)
 };
 
@@ -123,6 +127,14 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   const __nv_bfloat16 ha = __float2bfloat16_rn(a), hb = __float2bfloat16_rn(b);
   return (uint32_t)__bfloat16_as_ushort(ha) | ((uint32_t)__bfloat16_as_ushort(hb) << 16);
 }
+// (a, b) -> packed bf16x2 hi = rn(a, b), lo = rn(a - hi_a, b - hi_b); low half = a
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 __device__ __forceinline__ void split_bf16(float v, float& hi, float& lo) {
   hi = __bfloat162float(__float2bfloat16_rn(v));
   lo = v - hi;
@@ -175,16 +187,23 @@ __global__ void k_tc_images(const float2* __restrict__ taps, int taps_per_t, TcP
 //   (tile0, A_J) (tile1, A_J) (tile0, D_J) (tile1, D_J) ... (tile0, D_1) (tile1, D_1)
 // so the epilogue of one unit overlaps the MMAs of the next, and (a_shared) each
 // template K step in the ring feeds both units of a pair.
-//   warp 0    : bulk-copy producer of the template operand ring
-//   warp 1    : MMA issuer (one thread)
-//   warps 2-3 : Z builders: band segment -> smem staging (bulk copy), split into
-//               bf16 hi/lo 16-byte rows (double-buffered Z)
-//   warps 4-7 : epilogue: TMEM -> registers (tcgen05.ld), corr_s stores through a
-//               per-warp shared-memory transpose (whole 128-byte lines per store
-//               instruction), fused per-tile peak partials
+//   warp 0     : bulk-copy producer of the template operand ring
+//   warp 1     : MMA issuer (one thread)
+//   warps 2-5  : Z builders: band segment -> smem staging (bulk copy), split into
+//                bf16 hi/lo 16-byte rows (double-buffered Z)
+//   warps 6-13 : epilogue, two warps per TMEM lane group (4 x 32-lag chunks each):
+//                tcgen05.ld (next chunk prefetched), complex interleave through a
+//                per-warp shared-memory transpose, one 256-byte template row per
+//                store instruction, fused peak partials (|.|^2 max per chunk)
 // ---------------------------------------------------------------------------
 constexpr int kTcNZB = 2;                 // Z buffers
-constexpr int kTcEpiPitch = 272;          // bytes per template row of the epilogue transpose (256 + 16)
+constexpr int kTcBuildWarps = 5;
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcEpiBytes = 8192;         // per epilogue warp: 2 buffers x two 16 x 16 x 8 B TMA boxes (128B swizzle)
+constexpr int kTcFirstBuild = 3;         // warp 2: band stager
+constexpr int kTcFirstEpi = kTcFirstBuild + kTcBuildWarps;
+constexpr int kTcWarps = kTcFirstEpi + kTcEpiWarps;
+constexpr int kTcThreads = 32 * kTcWarps;
 
 struct TcSmem {
   int ring, zbuf, stg, epi, total;
@@ -192,27 +211,52 @@ struct TcSmem {
 __host__ __device__ inline TcSmem tc_smem_layout(const TcParams& p) {
   TcSmem m;
   m.ring = 1024;
-  m.zbuf = m.ring + p.stages * 8192;
+  m.zbuf = m.ring + p.stages * kTcStageBytes;
   m.stg = m.zbuf + kTcNZB * 4 * p.nz_max * 16;
-  m.epi = m.stg + 2 * 2 * p.stg_len * 4;
-  m.total = m.epi + 4 * 16 * kTcEpiPitch;
+  m.epi = (m.stg + 2 * 2 * p.stg_len * 4 + 1023) & ~1023;      // 1024-aligned (128B swizzle atoms)
+  m.total = m.epi + kTcEpiWarps * kTcEpiBytes;
   return m;
 }
 
-struct TcUnit { long long row; int mt, tile, step, half; };
+struct TcUnit { int row, mt, tile, step, half; };
 
-__device__ __forceinline__ TcUnit tc_unit(const TcParams& p, long long pair, int k) {
-  // k = step * 2 + half within the pair
+__device__ __forceinline__ TcUnit tc_unit(const TcParams& p, int pair, int k) {
+  // k = step * 2 + half within the pair; 32-bit arithmetic (npairs < 2^30, host-checked)
   TcUnit u;
   u.step = k >> 1;
   u.half = k & 1;
-  const long long tg = 2 * pair + u.half;
-  u.tile = (int)(tg % p.ntiles);
-  const long long bt = tg / p.ntiles;
-  u.mt = (int)(bt % p.n_mt);
+  const int tp = p.ntiles >> 1;                                 // tile pairs per (row, template tile)
+  const int bt = pair / tp;
+  u.tile = 2 * (pair - bt * tp) + u.half;
   u.row = bt / p.n_mt;
+  u.mt = bt - u.row * p.n_mt;
   return u;
 }
+
+// mbarrier wait that suspends the warp (time hint) instead of spinning, so waiting
+// roles do not take issue slots from the epilogue warps sharing their SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
+}
+
+// Waits of the role pipeline; with -DSIDWT_TC_PROFILE they are timed (clock64) and
+// CTA 0 prints per-role totals when SIDWT_TC_PROF is set.
+#ifdef SIDWT_TC_PROFILE
+#define TC_TWAIT(bar, par, acc)                                   \
+  do {                                                            \
+    const long long _t0 = clock64();                              \
+    mbar_wait(bar, par);                                          \
+    acc += clock64() - _t0;                                       \
+  } while (0)
+#define TC_CLOCK() clock64()
+#else
+#define TC_TWAIT(bar, par, acc) mbar_wait(bar, par)
+#define TC_CLOCK() 0LL
+#endif
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" :: "r"(smem_u32(bar)) : "memory");
@@ -220,10 +264,36 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" :: "r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// wait for this thread's outstanding tcgen05.ld; the registers of `r` are tied to the
+// wait so no use of them can be scheduled before it
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :: "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t saddr, int x0, int x1, int x2, int x3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n"
+               :: "l"(map), "r"(saddr), "r"(x0), "r"(x1), "r"(x2), "r"(x3) : "memory");
+}
 
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict__ img, float2* __restrict__ corr,
-               PeakF* __restrict__ partials, TcParams p) {
+               PeakF* __restrict__ partials, const __grid_constant__ TcParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const TcSmem L = tc_smem_layout(p);
   const int S = p.stages;
@@ -234,7 +304,8 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
   uint64_t* accfull = zempty + 2;                               // [2]
   uint64_t* accempty = accfull + 2;                             // [2]
   uint64_t* stgbar = accempty + 2;                              // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(stgbar + 2);
+  uint64_t* stgempty = stgbar + 2;                              // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(stgempty + 2);
   unsigned char* ring = smem_raw + L.ring;
   unsigned char* zbuf = smem_raw + L.zbuf;
   float* stg = reinterpret_cast<float*>(smem_raw + L.stg);
@@ -245,11 +316,12 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&zfull[b], 64);
+      mbar_init(&zfull[b], 32 * kTcBuildWarps);
       mbar_init(&zempty[b], 1);
       mbar_init(&accfull[b], 1);
-      mbar_init(&accempty[b], 4);
+      mbar_init(&accempty[b], kTcEpiWarps);
       mbar_init(&stgbar[b], 1);
+      mbar_init(&stgempty[b], kTcBuildWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -259,106 +331,156 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
+  // Template-operand ring schedule per (tile pair, term) with K = ksteps: the first unit
+  // consumes K steps; the second reuses the last R = min(K, S) of them from the ring
+  // (resident) and reloads steps 0 .. K - R - 1; the ring index advances by 2K - R.
+  // First unit releases steps 0 .. K - R - 1, the second everything it consumes.
+  auto ring_at = [&](int s0, uint32_t ph0, int i, int& s_, uint32_t& ph_) {
+    s_ = s0 + i;
+    ph_ = ph0;
+    while (s_ >= S) { s_ -= S; ph_ ^= 1u; }
+  };
   if (warp == 0) {
     // ===================== template operand producer =====================
     if (lane == 0) {
-      long long n = 0;                                          // ring load counter
-      for (long long pair = blockIdx.x; pair < p.npairs; pair += gridDim.x) {
-        const int mt = (int)(((2 * pair) / p.ntiles) % p.n_mt);
+      long long w_empty = 0, t_start = TC_CLOCK();
+      int s = 0;
+      uint32_t ph = 0;                                          // slot / phase parity of the ring head
+      for (int pair = blockIdx.x; pair < (int)p.npairs; pair += gridDim.x) {
+        const int mt = (pair / (p.ntiles >> 1)) % p.n_mt;
         const unsigned char* img_mt = img + (size_t)mt * p.total_ksteps * 8192;
-        for (int k = 0; k < units_per_pair; ++k) {
-          if (p.a_shared && (k & 1)) continue;                  // second unit reuses the stages
-          const TcTerm& tm = p.term[k >> 1];
-          for (int kk = 0; kk < tm.ksteps; ++kk, ++n) {
-            const int s = (int)(n % S);
-            mbar_wait(&empty[s], (uint32_t)(((n / S) & 1) ^ 1));
-            mbar_expect_tx(&full[s], 8192);
-            bulk_load_g2s(ring + s * 8192, img_mt + (size_t)(tm.kofs + kk) * 8192, 8192, &full[s]);
+        for (int step = 0; step <= p.J; ++step) {
+          const TcTerm& tm = p.term[step];
+          const int K = tm.ksteps >> 1;                          // stages (two K steps each)
+          const int R = p.a_shared ? min(K, S) : 0;
+          const unsigned char* src = img_mt + (size_t)tm.kofs * 8192;
+          for (int i = 0; i < 2 * K - R; ++i) {
+            const int kk = i < K ? i : i - K;
+            TC_TWAIT(&empty[s], ph ^ 1u, w_empty);
+            mbar_expect_tx(&full[s], kTcStageBytes);
+            bulk_load_g2s(ring + s * kTcStageBytes, src + (size_t)kk * kTcStageBytes, kTcStageBytes, &full[s]);
+            if (++s == S) { s = 0; ph ^= 1u; }
           }
         }
       }
+      if (p.prof && blockIdx.x == 0)
+        printf("[tc prof] producer: total %lld  wait_empty %lld\n", TC_CLOCK() - t_start, w_empty);
     }
     __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
-      const uint32_t ring_a = smem_u32(ring), z_a = smem_u32(zbuf);
-      long long n = 0;                                          // ring consume counter
+      long long w_z = 0, w_acc = 0, w_full = 0, t_start = TC_CLOCK();
+      const uint64_t desc_ring = smem_desc(smem_u32(ring), 128, 256);
+      int s = 0;                                                // ring head slot / parity
+      uint32_t ph = 0;
       long long u = 0;                                          // unit counter
-      for (long long pair = blockIdx.x; pair < p.npairs; pair += gridDim.x) {
-        for (int k = 0; k < units_per_pair; ++k, ++u) {
-          const int step = k >> 1, a = k & 1, zb = (int)(u & 1);
+      for (int pair = blockIdx.x; pair < (int)p.npairs; pair += gridDim.x) {
+        for (int step = 0; step <= p.J; ++step) {
           const TcTerm& tm = p.term[step];
-          mbar_wait(&zfull[zb], (uint32_t)((u >> 1) & 1));
-          mbar_wait(&accempty[a], (uint32_t)(((u >> 1) & 1) ^ 1));
-          tc_fence_after();
+          const int K = tm.ksteps >> 1;                          // stages (two K steps each)
+          const int R = p.a_shared ? min(K, S) : 0;
           const int kbpp = tm.kp / 16;
           const uint32_t sbo_b = 128u / (uint32_t)tm.ge;
-          const uint32_t zbase = z_a + zb * 4 * zplane;
-          const uint32_t d = tbase + a * 256;
-          const bool wait_full = !p.a_shared || a == 0;
-          const bool release = !p.a_shared || a == 1;
-          const long long n0 = (p.a_shared && a == 1) ? n - tm.ksteps : n;
-          for (int kk = 0; kk < tm.ksteps; ++kk) {
-            const long long nn = n0 + kk;
-            const int s = (int)(nn % S);
-            if (wait_full) {
-              mbar_wait(&full[s], (uint32_t)((nn / S) & 1));
-              tc_fence_after();
+          for (int a = 0; a < 2; ++a, ++u) {
+            const int zb = (int)(u & 1);
+            TC_TWAIT(&zfull[zb], (uint32_t)((u >> 1) & 1), w_z);
+            TC_TWAIT(&accempty[a], (uint32_t)(((u >> 1) & 1) ^ 1), w_acc);
+            tc_fence_after();
+            const uint64_t desc_z = smem_desc(smem_u32(zbuf) + zb * 4 * zplane, 128, sbo_b);
+            const uint32_t d = tbase + a * 256;
+            bool first = step == 0;
+            for (int n = 0; n < K; ++n) {
+              // ring offset and stage of the n-th stage of this unit
+              int off, kq;
+              bool wait_full, release;
+              if (a == 0) { off = n; kq = n; wait_full = true; release = n < K - R; }
+              else if (n < R) { off = K - R + n; kq = K - R + n; wait_full = false; release = true; }
+              else { off = K + (n - R); kq = n - R; wait_full = true; release = true; }
+              int ss;
+              uint32_t pp;
+              ring_at(s, ph, off, ss, pp);
+              if (wait_full) {
+                TC_TWAIT(&full[ss], pp, w_full);
+                tc_fence_after();
+              }
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int kk = 2 * kq + h;
+                const int pl = kk >= kbpp, kb = kk - pl * kbpp;
+                const uint64_t dah = desc_ring + (uint64_t)((ss * kTcStageBytes + h * 8192) >> 4);
+                const uint64_t dal = dah + (4096 >> 4);
+                const uint64_t dbh = desc_z + (uint64_t)(((pl * 2 + 0) * zplane + kb * 256) >> 4);
+                const uint64_t dbl = desc_z + (uint64_t)(((pl * 2 + 1) * zplane + kb * 256) >> 4);
+                if (!(p.prof & 4)) {
+                  umma_bf16(d, dah, dbh, kTcIdesc, first ? 0u : 1u);
+                  umma_bf16(d, dah, dbl, kTcIdesc, 1u);
+                  umma_bf16(d, dal, dbh, kTcIdesc, 1u);
+                }
+                first = false;
+              }
+              if (release) umma_commit(&empty[ss]);
             }
-            const uint32_t a_hi = ring_a + s * 8192, a_lo = a_hi + 4096;
-            const int pl = kk / kbpp, kb = kk % kbpp;
-            const uint32_t zh = zbase + (pl * 2 + 0) * zplane + kb * 256;
-            const uint32_t zl = zbase + (pl * 2 + 1) * zplane + kb * 256;
-            const uint64_t dah = smem_desc(a_hi, 128, 256), dal = smem_desc(a_lo, 128, 256);
-            const uint64_t dbh = smem_desc(zh, 128, sbo_b), dbl = smem_desc(zl, 128, sbo_b);
-            umma_bf16(d, dah, dbh, kTcIdesc, (step == 0 && kk == 0) ? 0u : 1u);
-            umma_bf16(d, dah, dbl, kTcIdesc, 1u);
-            umma_bf16(d, dal, dbh, kTcIdesc, 1u);
-            if (release) umma_commit(&empty[s]);
+            umma_commit(&accfull[a]);
+            umma_commit(&zempty[zb]);
           }
-          if (!p.a_shared || a == 0) n += tm.ksteps;
-          umma_commit(&accfull[a]);
-          umma_commit(&zempty[zb]);
+          int ns;
+          uint32_t np;
+          ring_at(s, ph, 2 * K - R, ns, np);
+          s = ns; ph = np;
+        }
+      }
+      if (p.prof && blockIdx.x == 0)
+        printf("[tc prof] mma: total %lld  wait_z %lld  wait_acc %lld  wait_full %lld  units %lld\n",
+               TC_CLOCK() - t_start, w_z, w_acc, w_full, u);
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    // ===================== band stager (one thread) =====================
+    // Unit u's band segment (both planes) -> staging buffer u & 1 by two bulk copies
+    // (symmetric extension: contiguous, margins present), once the builders released it.
+    if (lane == 0 && p.ext != 0) {
+      long long u = 0;
+      for (int pair = blockIdx.x; pair < (int)p.npairs; pair += gridDim.x) {
+        const TcUnit u0 = tc_unit(p, pair, 0);
+        const float* brow_ = bands + (size_t)u0.row * (p.J + 1) * 2 * p.stride;
+        for (int k = 0; k < units_per_pair; ++k, ++u) {
+          const int sb = (int)(u & 1);
+          const TcTerm& tm = p.term[k >> 1];
+          const int pos0 = (u0.tile + (k & 1)) * 256 + tm.g * tm.kmin;
+          const int a = pos0 + p.ML;
+          const int a4 = a & ~3;
+          const int need = (a - a4) + tm.ge * (tm.nz - 1) + 8;
+          int len = (need + 3) & ~3;
+          if (a4 + len > p.stride) len = p.stride - a4;
+          const float* src = brow_ + (size_t)tm.band * 2 * p.stride + a4;
+          float* dst = stg + (size_t)sb * 2 * p.stg_len;
+          mbar_wait_sleep(&stgempty[sb], (uint32_t)(((u >> 1) & 1) ^ 1));
+          mbar_expect_tx(&stgbar[sb], (uint32_t)(2 * len * 4));
+          bulk_load_g2s(dst, src, (uint32_t)(len * 4), &stgbar[sb]);
+          bulk_load_g2s(dst + p.stg_len, src + p.stride, (uint32_t)(len * 4), &stgbar[sb]);
         }
       }
     }
     __syncwarp();
-  } else if (warp < 4) {
-    // ===================== Z builders (64 threads) =====================
-    const int bt = threadIdx.x - 64;
-    auto stage_band = [&](long long pair, int k, int sb) {
-      // symmetric extension: contiguous band segment -> stg[sb] by two bulk copies
-      const TcUnit un = tc_unit(p, pair, k);
-      const TcTerm& tm = p.term[un.step];
-      const int pos0 = un.tile * 256 + tm.g * tm.kmin;
-      const int a = pos0 + p.ML;
-      const int a4 = a & ~3;
-      const int need = (a - a4) + tm.ge * (tm.nz - 1) + 8;
-      int len = (need + 3) & ~3;
-      if (a4 + len > p.stride) len = p.stride - a4;
-      const float* src = bands + ((size_t)un.row * (p.J + 1) + tm.band) * 2 * p.stride + a4;
-      float* dst = stg + (size_t)sb * 2 * p.stg_len;
-      mbar_expect_tx(&stgbar[sb], (uint32_t)(2 * len * 4));
-      bulk_load_g2s(dst, src, (uint32_t)(len * 4), &stgbar[sb]);
-      bulk_load_g2s(dst + p.stg_len, src + p.stride, (uint32_t)(len * 4), &stgbar[sb]);
-    };
+  } else if (warp < kTcFirstEpi) {
+    // ===================== Z builders =====================
+    // Z[zb][plane][split][j] (16 bytes) = bf16 hi / lo of band[pos0 + ge j .. + 7]; four
+    // threads per row (two elements each), rows of both planes spread over the builders.
+    constexpr int NB = 32 * kTcBuildWarps;
+    const int bt = threadIdx.x - 32 * kTcFirstBuild;
+    const int e2 = bt & 3;                                      // element pair of the row
+    const int rb = bt >> 2;                                     // first row of this thread
+    constexpr int RS = NB / 4;                                  // row step
     const bool sym = p.ext != 0;
+    long long w_stg = 0, w_ze = 0, t_start = TC_CLOCK(), b_conv = 0;
     long long u = 0;
-    long long first_pair = blockIdx.x;
-    if (sym && bt == 0 && first_pair < p.npairs) stage_band(first_pair, 0, 0);
-    for (long long pair = blockIdx.x; pair < p.npairs; pair += gridDim.x) {
+    for (int pair = blockIdx.x; pair < (int)p.npairs; pair += gridDim.x) {
       for (int k = 0; k < units_per_pair; ++k, ++u) {
         const int zb = (int)(u & 1), sb = (int)(u & 1);
-        // prefetch the next unit's band segment
-        if (sym && bt == 0) {
-          long long np = pair;
-          int nk = k + 1;
-          if (nk == units_per_pair) { nk = 0; np = pair + gridDim.x; }
-          if (np < p.npairs) stage_band(np, nk, sb ^ 1);
-        }
         const TcUnit un = tc_unit(p, pair, k);
-        const TcTerm& tm = p.term[un.step];
+        const TcTerm tm = p.term[un.step];                      // by value: fields in registers
+        const int ge = tm.ge, nz = tm.nz;
         const int pos0 = un.tile * 256 + tm.g * tm.kmin;
         float* sp = stg + (size_t)sb * 2 * p.stg_len;
         int off, lim;
@@ -366,131 +488,202 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
           const int a = pos0 + p.ML;
           const int a4 = a & ~3;
           off = a - a4;
-          const int need = off + tm.ge * (tm.nz - 1) + 8;
+          const int need = off + ge * (nz - 1) + 8;
           int len = (need + 3) & ~3;
           if (a4 + len > p.stride) len = p.stride - a4;
           lim = len - 1;
-          mbar_wait(&stgbar[sb], (uint32_t)((u >> 1) & 1));
+          TC_TWAIT(&stgbar[sb], (uint32_t)((u >> 1) & 1), w_stg);
         } else {
-          // periodic: wrapped gather into the staging buffer
+          // periodic: wrapped gather into the staging buffer (builders themselves)
           off = 0;
-          const int need = tm.ge * (tm.nz - 1) + 8;
+          const int need = ge * (nz - 1) + 8;
           lim = need - 1;
           const float* b0 = bands + ((size_t)un.row * (p.J + 1) + tm.band) * 2 * p.stride;
-          for (int i = bt; i < need; i += 64) {
+          for (int i = bt; i < need; i += NB) {
             const int idx = (pos0 + i) & (p.N - 1);
             sp[i] = __ldg(b0 + idx);
             sp[p.stg_len + i] = __ldg(b0 + p.stride + idx);
           }
-          named_bar(1, 64);
+          named_bar(1, NB);
         }
-        mbar_wait(&zempty[zb], (uint32_t)(((u >> 1) & 1) ^ 1));
+        TC_TWAIT(&zempty[zb], (uint32_t)(((u >> 1) & 1) ^ 1), w_ze);
+        const long long _b1 = TC_CLOCK();
         unsigned char* zb_ptr = zbuf + zb * 4 * zplane;
-        for (int it = bt; it < 2 * tm.nz; it += 64) {
-          const int pl = it >= tm.nz;
-          const int j = it - pl * tm.nz;
-          const float* src = sp + pl * p.stg_len;
-          const int i0 = off + tm.ge * j;
-          float v[8];
+        const int nfast = min(nz, max(0, (lim - 7 - off) / ge + 1));   // rows needing no clamp
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = src[min(i0 + e, lim)];
-          uint32_t hw[4], lw[4];
+        for (int pl = 0; pl < 2; ++pl) {
+          const float* src = sp + pl * p.stg_len + off + 2 * e2;
+          uint32_t* zh = reinterpret_cast<uint32_t*>(zb_ptr + (pl * 2 + 0) * zplane) + e2;
+          uint32_t* zl = reinterpret_cast<uint32_t*>(zb_ptr + (pl * 2 + 1) * zplane) + e2;
+          int j = rb;
+          for (; j + 3 * RS < nfast; j += 4 * RS) {
+            float x0[4], x1[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float h0, l0, h1, l1;
-            split_bf16(v[2 * e], h0, l0);
-            split_bf16(v[2 * e + 1], h1, l1);
-            hw[e] = pack_bf16x2(h0, h1);
-            lw[e] = pack_bf16x2(l0, l1);
+            for (int q = 0; q < 4; ++q) { x0[q] = src[ge * (j + q * RS)]; x1[q] = src[ge * (j + q * RS) + 1]; }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t hw, lw;
+              split_bf16x2(x0[q], x1[q], hw, lw);
+              zh[(j + q * RS) * 4] = hw;
+              zl[(j + q * RS) * 4] = lw;
+            }
           }
-          *reinterpret_cast<uint4*>(zb_ptr + (pl * 2 + 0) * zplane + j * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          *reinterpret_cast<uint4*>(zb_ptr + (pl * 2 + 1) * zplane + j * 16) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          for (; j < nz; j += RS) {
+            const int i0 = off + ge * j + 2 * e2;
+            const float x0 = sp[pl * p.stg_len + min(i0, lim)];
+            const float x1 = sp[pl * p.stg_len + min(i0 + 1, lim)];
+            uint32_t hw, lw;
+            split_bf16x2(x0, x1, hw, lw);
+            zh[j * 4] = hw;
+            zl[j * 4] = lw;
+          }
         }
         fence_proxy_async_smem();
         mbar_arrive(&zfull[zb]);
-        named_bar(1, 64);                                       // staging buffer free for the next prefetch
+        __syncwarp();
+        if (sym && lane == 0) mbar_arrive(&stgempty[sb]);       // staging buffer free
+        if (!sym) named_bar(1, NB);
+        b_conv += TC_CLOCK() - _b1;
       }
     }
+    if (p.prof && blockIdx.x == 0 && bt == 0)
+      printf("[tc prof] builder: total %lld  wait_stg %lld  wait_zempty %lld  convert %lld\n",
+             TC_CLOCK() - t_start, w_stg, w_ze, b_conv);
   } else {
-    // ===================== epilogue (warps 4-7, TMEM lane group = warp & 3) =====================
+    // ===================== epilogue (8 warps; TMEM lane group = warp & 3) =====================
+    // Lane pair (2 r, 2 r + 1) holds re / im of template row r for 32 lags per chunk.  One
+    // shuffle exchange gives each lane 16 complex values in "slots": even lane slot i =
+    // lag i, odd lane slot i = lag 16 + (i ^ 8).  They go to a per-warp staging area (two
+    // buffers, alternating per chunk) of two TMA boxes (lags 0-15 / 16-31) of 16 template
+    // rows x 128 B, 128B-swizzled: chunk q of row r at (q ^ (r & 7)); the slot rotation
+    // makes every quarter-warp's 16-byte stores hit 8 distinct bank groups.  A 4-D TMA
+    // tensor store per box writes corr (coalesced 128-byte rows, out-of-range templates
+    // clipped).  Peaks: |.|^2 max per chunk from the registers; the value at the winning
+    // lag is read back from the staging buffer.
+    const int ew = warp - kTcFirstEpi;
     const int lg = warp & 3;
-    unsigned char* epi = smem_raw + L.epi + lg * 16 * kTcEpiPitch;
-    const int tl = lg * 16 + (lane >> 1);                       // template within the tile
+    const int hh = ew >> 2;                                     // column half: chunks 4 hh .. 4 hh + 3
+    unsigned char* epi = smem_raw + L.epi + ew * kTcEpiBytes;
+    const int r = lane >> 1;                                    // template row of this lane pair
     const bool odd = lane & 1;
+    const int woff = (odd ? 2048 : 0) + r * 128;
+    const int sw = (r & 7) ^ (odd ? 4 : 0);                     // chunk q -> physical q ^ sw
+    long long w_acc = 0, t_start = TC_CLOCK(), e_bw = 0, e_ld = 0, e_st = 0;
     long long u = 0;
-    for (long long pair = blockIdx.x; pair < p.npairs; pair += gridDim.x) {
+    for (int pair = blockIdx.x; pair < (int)p.npairs; pair += gridDim.x) {
       for (int k = 0; k < units_per_pair; ++k, ++u) {
         const TcUnit un = tc_unit(p, pair, k);
         const int a = k & 1;
         const int ti = p.J - un.step;
-        const int t = un.mt * kTcTemplates + tl;
-        const bool valid = t < p.n_t;
-        const int tau_tile = un.tile * 256;
-        mbar_wait(&accfull[a], (uint32_t)((u >> 1) & 1));
+        const int t0 = un.mt * kTcTemplates + lg * 16;
+        const bool valid = t0 + r < p.n_t;
+        const int tau_h = un.tile * 256 + hh * 128;
+        TC_TWAIT(&accfull[a], (uint32_t)((u >> 1) & 1), w_acc);
         tc_fence_after();
-        PeakF best;
-        best.m2 = -1.f; best.tau = 0x7fffffff; best.re = 0.f; best.im = 0.f;
+        if (p.prof & 2) {                                       // debug: skip the epilogue work
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&accempty[a]);
+          continue;
+        }
+        float bm2 = -1.f, bre = 0.f, bim = 0.f;
+        int btau = 0x7fffffff;
+        const uint32_t tcol = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * 256 + hh * 128);
 #pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
-          float v[32];
-          tmem_ld32(tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * 256 + c * 32), v);
-          if (c == 7) {                                         // accumulator fully read: release it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&accempty[a]);
-          }
-          float x[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) x[i] = __shfl_xor_sync(0xffffffffu, odd ? v[i] : v[16 + i], 1);
-          // even lane: lags c*32 + 0..15 = (v[i], x[i]); odd lane: c*32 + 16.. = (x[i], v[16+i])
-          float re[16], im[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) { re[i] = odd ? x[i] : v[i]; im[i] = odd ? v[16 + i] : x[i]; }
-          const int tau = tau_tile + c * 32 + (odd ? 16 : 0);
-          if (p.want_peaks && valid) {
+        for (int c2 = 0; c2 < 2; ++c2) {
+          // two 32-lag chunks per staging fill: one proxy fence and one TMA group per 64 lags
+          const long long _e1 = TC_CLOCK();
+          if (lane == 0) bulk_wait_read_all();                  // previous group has read the staging
+          __syncwarp();
+          e_bw += TC_CLOCK() - _e1;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            const int c = 2 * c2 + h;
+            uint32_t v[32];
+            const long long _e0 = TC_CLOCK();
+            tmem_ld32_nowait(tcol + c * 32, v);
+            tmem_wait_ld(v);
+            e_ld += TC_CLOCK() - _e0;
+            if (c == 3) {                                       // accumulator fully read: release it
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&accempty[a]);
+            }
+            float mine[16], other[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const float m2 = mag2f(re[i], im[i]);
-              if (m2 > best.m2) { best.m2 = m2; best.tau = tau + i; best.re = re[i]; best.im = im[i]; }
+              const float send = __uint_as_float(odd ? v[i] : v[16 + (i ^ 8)]);
+              mine[i] = __uint_as_float(odd ? v[16 + (i ^ 8)] : v[i]);
+              other[i] = __shfl_xor_sync(0xffffffffu, send, 1);
             }
-          }
-          if (p.want_corr) {
-            // transpose: row (template) lane>>1, 16-byte chunks h*8 + i, chunk i >= 8 stored at (i ^ 4)
-            unsigned char* rowp = epi + (lane >> 1) * kTcEpiPitch;
+            unsigned char* buf = epi + h * 4096;
+            const int tau_c = tau_h + c * 32;
+            // (re, im) = (mine, other) on even lanes, (other, mine) on odd lanes
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int cl = (odd ? 8 : 0) + i;
-              const int cp = cl ^ (odd ? 4 : 0);
-              *reinterpret_cast<float4*>(rowp + cp * 16) = make_float4(re[2 * i], im[2 * i], re[2 * i + 1], im[2 * i + 1]);
+            for (int q = 0; q < 8; ++q) {
+              const float r0 = odd ? other[2 * q] : mine[2 * q], i0 = odd ? mine[2 * q] : other[2 * q];
+              const float r1 = odd ? other[2 * q + 1] : mine[2 * q + 1], i1 = odd ? mine[2 * q + 1] : other[2 * q + 1];
+              *reinterpret_cast<float4*>(buf + woff + ((q ^ sw) << 4)) = make_float4(r0, i0, r1, i1);
             }
-            __syncwarp();
-            // 8 instructions x 512 B: rows 2r, 2r+1 (lanes 0-15 / 16-31), chunk lane & 15
+            if (p.want_peaks && valid) {
+              float m2[16];
+              float mx = -1.f;
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              const int trow = 2 * r + (lane >> 4);
-              const int cl = lane & 15;
-              const int cp = cl ^ ((cl >> 3) << 2);
-              const float4 val = *reinterpret_cast<const float4*>(epi + trow * kTcEpiPitch + cp * 16);
-              const int tt = un.mt * kTcTemplates + lg * 16 + trow;
-              if (tt < p.n_t) {
-                float2* dst = corr + (((size_t)un.row * p.n_t + tt) * (p.J + 1) + ti) * p.N + tau_tile + c * 32;
-                reinterpret_cast<float4*>(dst)[cl] = val;
+              for (int i = 0; i < 16; ++i) { m2[i] = mag2f(mine[i], other[i]); mx = fmaxf(mx, m2[i]); }
+              if (mx > bm2) {
+                // smallest lag attaining mx: slot i <-> lag (odd ? 16 + (i ^ 8) : i)
+                int bl = 0x7fffffff;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const int lag = odd ? 16 + (i ^ 8) : i;
+                  bl = (m2[i] == mx) ? min(bl, lag) : bl;
+                }
+                // value from this thread's own staging write: row r, lag bl
+                const float2 z = *reinterpret_cast<const float2*>(
+                    buf + (bl >> 4) * 2048 + r * 128 + (((((bl & 15) >> 1) ^ (r & 7))) << 4) + (bl & 1) * 8);
+                bm2 = mx; btau = tau_c + bl; bre = z.x; bim = z.y;
               }
             }
-            __syncwarp();
           }
+          const long long _e2 = TC_CLOCK();
+          fence_proxy_async_smem();
+          __syncwarp();
+          // warp-uniform operands (broadcast, so the TMA operands live in uniform registers)
+          const int u_tau = __shfl_sync(0xffffffffu, tau_h + c2 * 64, 0);
+          const int u_ti = __shfl_sync(0xffffffffu, ti, 0);
+          const int u_t0 = __shfl_sync(0xffffffffu, t0, 0);
+          const int u_row = __shfl_sync(0xffffffffu, un.row, 0);
+          const uint32_t u_sa = __shfl_sync(0xffffffffu, smem_u32(epi), 0);
+          if (lane == 0) {
+            if (p.want_corr) {
+              tma_store_4d(&p.tmap, u_sa, u_tau, u_ti, u_t0, u_row);
+              tma_store_4d(&p.tmap, u_sa + 2048, u_tau + 16, u_ti, u_t0, u_row);
+              tma_store_4d(&p.tmap, u_sa + 4096, u_tau + 32, u_ti, u_t0, u_row);
+              tma_store_4d(&p.tmap, u_sa + 6144, u_tau + 48, u_ti, u_t0, u_row);
+            }
+            bulk_commit();
+          }
+          e_st += TC_CLOCK() - _e2;
         }
         if (p.want_peaks) {
-          PeakF o;
-          o.m2 = __shfl_xor_sync(0xffffffffu, best.m2, 1);
-          o.tau = __shfl_xor_sync(0xffffffffu, best.tau, 1);
-          o.re = __shfl_xor_sync(0xffffffffu, best.re, 1);
-          o.im = __shfl_xor_sync(0xffffffffu, best.im, 1);
-          if (beats(o.m2, o.tau, best.m2, best.tau)) best = o;
-          if (!odd && valid) partials[(((size_t)un.row * p.n_t + t) * (p.J + 1) + ti) * p.ntiles + un.tile] = best;
+          const float om2 = __shfl_xor_sync(0xffffffffu, bm2, 1);
+          const int otau = __shfl_xor_sync(0xffffffffu, btau, 1);
+          const float ore = __shfl_xor_sync(0xffffffffu, bre, 1);
+          const float oim = __shfl_xor_sync(0xffffffffu, bim, 1);
+          if (beats(om2, otau, bm2, btau)) { bm2 = om2; btau = otau; bre = ore; bim = oim; }
+          if (!odd && valid) {
+            PeakF b;
+            b.m2 = bm2; b.tau = btau; b.re = bre; b.im = bim;
+            partials[(((size_t)un.row * p.n_t + t0 + r) * (p.J + 1) + ti) * (2 * p.ntiles) + 2 * un.tile + hh] = b;
+          }
         }
       }
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+    if (p.prof && blockIdx.x == 0 && lane == 0)
+      printf("[tc prof] epilogue warp %d: total %lld  wait_accfull %lld  ldtm %lld  bulkwait %lld  sts+tma %lld\n", warp,
+             TC_CLOCK() - t_start, w_acc, e_ld, e_bw, e_st);
   }
   tc_fence_before();
   __syncthreads();

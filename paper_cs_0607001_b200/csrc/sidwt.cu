@@ -1,6 +1,8 @@
 // sidwt.cu -- host side of libsidwt: the C ABI declared in include/sidwt.h.
 // Plans, validation, template loading, layout, and launches of the sm_100a
 // kernels in kernels.cuh.  No computation of the path happens on the host.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -243,11 +245,12 @@ static void configure_tc(sidwt_plan_s* p) {
   t.stages = 0;
   const TcSmem base = tc_smem_layout(t);                  // with 0 stages
   const int budget = 227 * 1024;
-  const int fit = (budget - base.total) / 8192;
-  if (fit < 4) return;
+  const int fit = (budget - base.total) / kTcStageBytes;
+  if (fit < 3) return;
   t.stages = std::min(kTcMaxStages, fit);
-  t.a_shared = t.stages >= kmax ? 1 : 0;
-  if (const char* e = std::getenv("SIDWT_TC_SHARED")) t.a_shared = (atoi(e) != 0) && t.a_shared;
+  t.a_shared = 1;                                         // second unit of a pair reuses resident K steps
+  if (const char* e = std::getenv("SIDWT_TC_SHARED")) t.a_shared = atoi(e) != 0;
+  if (const char* e = std::getenv("SIDWT_TC_STAGES")) t.stages = std::max(3, std::min(t.stages, atoi(e)));
   p->tc_smem = (size_t)tc_smem_layout(t).total;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -372,7 +375,7 @@ sidwt_status sidwt_analyze(sidwt_plan p, const void* d_rows, int64_t rows, void*
 
 static sidwt_status ensure_partials(sidwt_plan_s* p) {
   const size_t rec = is_int(p) ? sizeof(PeakI) : sizeof(PeakF);
-  const size_t need = (size_t)p->batch * p->n_t * (p->J + 1) * (p->tc ? p->tcp.ntiles : p->cor.ntiles) * rec;
+  const size_t need = (size_t)p->batch * p->n_t * (p->J + 1) * (p->tc ? 2 * p->tcp.ntiles : p->cor.ntiles) * rec;
   if (p->partials_bytes >= need) return SIDWT_OK;
   if (p->d_partials) cudaFree(p->d_partials);
   p->d_partials = nullptr;
@@ -383,6 +386,25 @@ static sidwt_status ensure_partials(sidwt_plan_s* p) {
   return SIDWT_OK;
 }
 
+// corr [rows][n_t][J+1][N] complex64 as a 4-D TMA tensor of 8-byte elements; box = 16 lags x
+// 1 scale x 16 templates x 1 row, 128-byte swizzle (matches the epilogue staging layout).
+static bool encode_corr_map(CUtensorMap* map, void* corr, int64_t rows, const sidwt_plan_s* p) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)p->N, (cuuint64_t)(p->J + 1), (cuuint64_t)p->n_t, (cuuint64_t)rows};
+  const cuuint64_t strides[3] = {(cuuint64_t)p->N * 8, (cuuint64_t)p->N * 8 * (p->J + 1),
+                                 (cuuint64_t)p->N * 8 * (p->J + 1) * p->n_t};
+  const cuuint32_t box[4] = {16, 1, 16, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, corr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static sidwt_status correlate_tc(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
                                  int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
   TcParams t = p->tcp;
@@ -390,6 +412,9 @@ static sidwt_status correlate_tc(sidwt_plan_s* p, const void* d_bands, int64_t r
   t.want_corr = d_corr != nullptr;
   t.want_peaks = peaks;
   t.npairs = rows * t.n_mt * t.ntiles / 2;
+  if (t.npairs >= (1LL << 30)) return SIDWT_ERR_RANGE;
+  if (d_corr && !encode_corr_map(&t.tmap, d_corr, rows, p)) return SIDWT_ERR_CUDA;
+  if (const char* e = std::getenv("SIDWT_TC_PROF")) t.prof = atoi(e);
   const int64_t grid = std::min<int64_t>(t.npairs, p->tc_sms);
   cudaError_t e = cudaFuncSetAttribute(k_correlate_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tc_smem);
   if (e == cudaSuccess) {
@@ -402,7 +427,7 @@ static sidwt_status correlate_tc(sidwt_plan_s* p, const void* d_bands, int64_t r
   p->last_launches = 1;
   if (e == cudaSuccess && peaks) {
     const int64_t count = rows * p->n_t * (p->J + 1);
-    k_peaks_finalize<false><<<(unsigned)cdiv(count, 256), 256, 0, s>>>(p->d_partials, t.ntiles, count, d_lag, d_val);
+    k_peaks_finalize<false><<<(unsigned)cdiv(count, 256), 256, 0, s>>>(p->d_partials, 2 * t.ntiles, count, d_lag, d_val);
     e = cudaGetLastError();
     p->last_launches = 2;
   }
