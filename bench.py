@@ -41,9 +41,10 @@ def load_peaks():
     try:
         with open(p) as f:
             d = json.load(f)
-        return dict(hbm=float(d["hbm_gbs"]), sm_mhz=float(d.get("sm_max_mhz", 1965.0)), src="measured")
+        return dict(hbm=float(d["hbm_gbs"]), sm_mhz=float(d.get("sm_max_mhz", 1965.0)),
+                    bf16_sustained=float(d.get("bf16_tflops_sustained", d.get("bf16_tflops", 1400.0))), src="measured")
     except Exception:
-        return dict(hbm=6650.0, sm_mhz=1965.0, src="fallback")
+        return dict(hbm=6650.0, sm_mhz=1965.0, bf16_sustained=1400.0, src="fallback")
 
 
 def fp32_peak_tflops(sm_mhz):
@@ -109,15 +110,18 @@ class ClockSampler:
 
 
 def algorithmic(cfg, plan):
-    """Per-row algorithmic bytes / flops of each kernel (DESIGN.md section 4)."""
+    """Per-row algorithmic bytes / flops of each kernel (DESIGN.md section 6)."""
     J, N = cfg.levels, cfg.N
     sb = 4 if cfg.is_int else 8
     stride = plan.band_stride
     k1_bytes = N * sb + (J + 1) * 2 * stride * 4
     taps = sum(c for c in plan_counts(plan))
-    k2_flops = cfg.n_templates * N * taps * 8            # 4 FFMA per complex MAC (8 flop)
+    k2_flops = cfg.n_templates * N * taps * 8            # complex MAC = 8 real flops
     k2_bytes = (J + 1) * 2 * stride * 4 + cfg.n_templates * (J + 1) * N * 8
     return dict(k1_bytes=k1_bytes, k2_flops=k2_flops, k2_bytes=k2_bytes, taps=taps)
+
+
+BF16_SPLIT_PRODUCTS = 3     # tensor-core bank path: fp32 = bf16 hi + lo, hi.hi + hi.lo + lo.hi
 
 
 def plan_counts(plan):
@@ -315,27 +319,40 @@ def main():
 
     pk = load_peaks()
     alg = algorithmic(cfg, plan)
+    tc = plan.uses_tensor_cores()
     k1_gbs = R * alg["k1_bytes"] / (k1_ms * 1e-3) / 1e9
     k2_tflops = R * alg["k2_flops"] / (k2_ms * 1e-3) / 1e12
     k2_gbs = R * alg["k2_bytes"] / (k2_ms * 1e-3) / 1e9
     fp32_peak = fp32_peak_tflops(pk["sm_mhz"])
+    k2_kernel = "k_correlate_tc" if tc else "k_correlate"
+    if tc:
+        # tensor pipe: the algorithmic complex MACs run as 3 bf16 products (split precision);
+        # peak = measured sustained cuBLAS bf16 (the kernel runs inside a long power-capped step)
+        comp = {"achieved": k2_tflops * BF16_SPLIT_PRODUCTS, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
+                "frac": k2_tflops * BF16_SPLIT_PRODUCTS / pk["bf16_sustained"], "flops_per_row": alg["k2_flops"],
+                "note": "bf16 tensor flops = 3 x algorithmic complex-MAC flops (hi.hi + hi.lo + lo.hi)",
+                "peak_source": f"{pk['src']} MEASURED_PEAKS.json bf16_tflops_sustained"}
+        comp_key, comp_bound = "tensor", "tensor"
+    else:
+        comp = {"achieved": k2_tflops, "peak": fp32_peak, "unit": "TFLOP/s", "frac": k2_tflops / fp32_peak,
+                "flops_per_row": alg["k2_flops"],
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x %.0f MHz" % pk["sm_mhz"]}
+        comp_key, comp_bound = "alu", "alu"
     stages = {
         "analyze": {"kernel": "k_analyze", "ms": k1_ms, "bound": "hbm", "achieved": k1_gbs, "peak": pk["hbm"],
                     "unit": "GB/s", "frac": k1_gbs / pk["hbm"], "bytes_per_row": alg["k1_bytes"]},
-        "correlate_peaks": {"kernel": "k_correlate+k_peaks_finalize", "ms": k2_ms,
-                            "alu": {"achieved": k2_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
-                                    "frac": k2_tflops / fp32_peak, "flops_per_row": alg["k2_flops"]},
+        "correlate_peaks": {"kernel": k2_kernel + "+k_peaks_finalize", "ms": k2_ms,
+                            comp_key: comp,
                             "hbm": {"achieved": k2_gbs, "peak": pk["hbm"], "unit": "GB/s",
                                     "frac": k2_gbs / pk["hbm"], "bytes_per_row": alg["k2_bytes"]}},
     }
     if k2_ms >= k1_ms:
-        a2, h2 = stages["correlate_peaks"]["alu"], stages["correlate_peaks"]["hbm"]
+        a2, h2 = stages["correlate_peaks"][comp_key], stages["correlate_peaks"]["hbm"]
         use = a2 if a2["frac"] >= h2["frac"] else h2
-        roof = {"kernel": "k_correlate", "bound": "alu" if use is a2 else "hbm", "achieved": use["achieved"],
+        roof = {"kernel": k2_kernel, "bound": comp_bound if use is a2 else "hbm", "achieved": use["achieved"],
                 "peak": use["peak"], "unit": use["unit"], "frac": use["frac"],
-                "traffic": traffic_from_profiles(cfg.name, "k_correlate"),
-                "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x %.0f MHz" % pk["sm_mhz"])
-                if use is a2 else f"{pk['src']} MEASURED_PEAKS.json hbm_gbs"}
+                "traffic": traffic_from_profiles(cfg.name, k2_kernel),
+                "peak_source": use["peak_source"] if use is a2 else f"{pk['src']} MEASURED_PEAKS.json hbm_gbs"}
     else:
         a1 = stages["analyze"]
         roof = {"kernel": "k_analyze", "bound": "hbm", "achieved": a1["achieved"], "peak": a1["peak"],
@@ -352,6 +369,7 @@ def main():
                        R * cfg.n_templates * (cfg.levels + 1) * cfg.N * 8 / 1e9)},
         "roofline": roof,
         "stages": stages,
+        "tensor_cores": tc,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }

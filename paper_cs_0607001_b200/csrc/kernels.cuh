@@ -358,11 +358,13 @@ __device__ __forceinline__ void bulk_load_g2s(void* sdst, const void* gsrc, uint
 // cooperative loads instead.
 // ---------------------------------------------------------------------------
 struct Term { int band, lg, kmin, npad, ntap, toff; };
+constexpr int kCTaps = 1536;     // template taps carried in the kernel parameters (constant cache)
 struct CorParams {
   int N, J, ext, stride, ML, n_t, TT, ntiles, taps_per_t, balloc, nbuf;
   long long rows;
   int want_corr, want_peaks;
   Term term[kMaxTerms];
+  uint2 ctap[kCTaps];            // [n_t][taps_per_t] float2 / int2 bits when n_t * taps_per_t <= kCTaps
 };
 
 // One chunk of REM taps (REM = Q except in an item's last chunk).  Step kk: every output
@@ -464,9 +466,12 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
   }
 }
 
-template <bool INT, int Q, int MINB>
+// CT: the taps are read from the kernel parameters (uniform constant-cache loads, LDCU),
+// keeping the shared-memory pipe for the band values: per tap and item 2 LDS feed 4Q FFMA.
+template <bool INT, int Q, int MINB, bool CT>
 __global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
-                                                   void* __restrict__ corr, void* __restrict__ partials, CorParams p) {
+                                                   void* __restrict__ corr, void* __restrict__ partials,
+                                                   const __grid_constant__ CorParams p) {
   typedef typename std::conditional<INT, int, float>::type T;
   typedef typename std::conditional<INT, int2, float2>::type T2;
   typedef typename std::conditional<INT, unsigned, float>::type A;
@@ -474,7 +479,7 @@ __global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict_
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);                 // [2]
   T2* stap = reinterpret_cast<T2*>(smem_raw + 16);
   T* sbuf = reinterpret_cast<T*>(smem_raw + 16 + (((size_t)p.taps_per_t * sizeof(T2) + 127) & ~(size_t)127));  // [2][2][balloc]
-  T* acc = sbuf + 2 * (size_t)p.nbuf * p.balloc;                          // [2 buffers][2 planes][TT]
+  T2* acc = reinterpret_cast<T2*>(sbuf + 2 * (size_t)p.nbuf * p.balloc);   // [2 buffers][TT] complex (re, im)
   constexpr int kWarps = 256 / 32;
   typedef typename std::conditional<INT, PeakI, PeakF>::type PK;
   __shared__ PK red[kMaxTerms][kWarps];
@@ -510,7 +515,9 @@ __global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict_
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   const T2* tsrc = static_cast<const T2*>(taps) + (size_t)t * p.taps_per_t;
-  for (int i = threadIdx.x; i < p.taps_per_t; i += blockDim.x) stap[i] = tsrc[i];
+  if (!CT)
+    for (int i = threadIdx.x; i < p.taps_per_t; i += blockDim.x) stap[i] = tsrc[i];
+  const T2* tbase = CT ? reinterpret_cast<const T2*>(p.ctap) + (size_t)t * p.taps_per_t : stap;
   __syncthreads();
   if (tma && threadIdx.x == 0) issue(0, 0);
   const bool dbl = p.nbuf == 2;
@@ -553,21 +560,37 @@ __global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict_
     // compute term, accumulate into acc[cur^1] = acc[cur] + term
     const int nq = TT >> tm.lg;
     const int nqb = (nq + Q - 1) / Q;
-    T* aprev = acc + (size_t)cur * 2 * TT;
-    T* anew = acc + (size_t)(cur ^ 1) * 2 * TT;
+    const T2* aprev = acc + (size_t)cur * TT;
+    T2* anew = acc + (size_t)(cur ^ 1) * TT;
     for (int w = threadIdx.x; w < g * nqb; w += blockDim.x) {
       const int r = w & (g - 1);
       const int q0 = (w >> tm.lg) * Q;
       A ar[Q], ai[Q];
-      corr_item<INT, Q>(sb, plane, stap + tm.toff, tm.ntap, r, tm.lg, q0, ar, ai);
+      corr_item<INT, Q>(sb, plane, tbase + tm.toff, tm.ntap, r, tm.lg, q0, ar, ai);
+      // eq. (4) suffix sum: corr_ti = corr_{ti+1} + term (outputs r + g (q0 + j))
+      const int base = r + (q0 << tm.lg);
+      const T2* pp = aprev + base;
+      T2* pn = anew + base;
+      const int nj = min(Q, nq - q0);
+      if (step == 0) {
 #pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        if (q0 + j < nq) {
-          const int tl = r + ((q0 + j) << tm.lg);
-          const A pr = step ? (A)aprev[tl] : A(0), pi = step ? (A)aprev[TT + tl] : A(0);
-          anew[tl] = (T)(pr + ar[j]);
-          anew[TT + tl] = (T)(pi + ai[j]);
+        for (int j = 0; j < Q; ++j)
+          if (j < nj) { T2 o; o.x = (T)ar[j]; o.y = (T)ai[j]; pn[j * g] = o; }
+      } else if (nj == Q) {
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          const T2 v = pp[j * g];
+          T2 o; o.x = (T)((A)v.x + ar[j]); o.y = (T)((A)v.y + ai[j]);
+          pn[j * g] = o;
         }
+      } else {
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+          if (j < nj) {
+            const T2 v = pp[j * g];
+            T2 o; o.x = (T)((A)v.x + ar[j]); o.y = (T)((A)v.y + ai[j]);
+            pn[j * g] = o;
+          }
       }
     }
     __syncthreads();
@@ -575,7 +598,7 @@ __global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict_
     cur ^= 1;
     // store corr_ti (4 lags per thread-iteration, 2 x 16-byte stores) and reduce this tile's
     // peak partial: lags increase within a thread, so a strict '>' keeps the smallest lag.
-    const T* a = acc + (size_t)cur * 2 * TT;
+    const T2* a = acc + (size_t)cur * TT;
     T2* dst = p.want_corr ? static_cast<T2*>(corr) + (((size_t)row * p.n_t + t) * (p.J + 1) + ti) * p.N + tau0 : nullptr;
     PK best;
     best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0;
@@ -590,29 +613,30 @@ __global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict_
         best.m2 = bt ? m : best.m2; best.tau = bt ? tau : best.tau; best.re = bt ? re : best.re; best.im = bt ? im : best.im;
       }
     };
-    if ((TT & 3) == 0) {
-      for (int tl = threadIdx.x * 4; tl < TT; tl += blockDim.x * 4) {
-        typedef typename std::conditional<INT, int4, float4>::type T4;
-        const T4 vr = *reinterpret_cast<const T4*>(a + tl);
-        const T4 vi = *reinterpret_cast<const T4*>(a + TT + tl);
-        if (dst) {
-          T4 o0, o1;
-          o0.x = vr.x; o0.y = vi.x; o0.z = vr.y; o0.w = vi.y;
-          o1.x = vr.z; o1.y = vi.z; o1.z = vr.w; o1.w = vi.w;
-          *reinterpret_cast<T4*>(dst + tl) = o0;
-          *reinterpret_cast<T4*>(dst + tl + 2) = o1;
-        }
+    if ((TT & 1) == 0) {
+      // two lags per 16-byte load / store, straight copy of the interleaved accumulator
+      typedef typename std::conditional<INT, int4, float4>::type T4;
+      for (int tl = threadIdx.x * 2; tl < TT; tl += blockDim.x * 2) {
+        const T4 v = *reinterpret_cast<const T4*>(a + tl);
+        if (dst) *reinterpret_cast<T4*>(dst + tl) = v;
         if (p.want_peaks) {
-          consider(vr.x, vi.x, tau0 + tl);
-          consider(vr.y, vi.y, tau0 + tl + 1);
-          consider(vr.z, vi.z, tau0 + tl + 2);
-          consider(vr.w, vi.w, tau0 + tl + 3);
+          if constexpr (INT) {
+            consider(v.x, v.y, tau0 + tl);
+            consider(v.z, v.w, tau0 + tl + 1);
+          } else {
+            const float m0 = mag2f(v.x, v.y), m1 = mag2f(v.z, v.w);
+            const float mx = fmaxf(m0, m1);
+            if (best.tau < 0 || mx > best.m2) {
+              const bool k0 = m0 == mx;
+              best.m2 = mx; best.tau = tau0 + tl + (k0 ? 0 : 1);
+              best.re = k0 ? v.x : v.z; best.im = k0 ? v.y : v.w;
+            }
+          }
         }
       }
     } else {
       for (int tl = threadIdx.x; tl < TT; tl += blockDim.x) {
-        T2 v;
-        v.x = a[tl]; v.y = a[TT + tl];
+        const T2 v = a[tl];
         if (dst) dst[tl] = v;
         if (p.want_peaks) consider(v.x, v.y, tau0 + tl);
       }

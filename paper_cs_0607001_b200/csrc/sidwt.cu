@@ -53,6 +53,7 @@ struct sidwt_plan_s {
   void *w_rows = nullptr, *w_bands = nullptr, *w_corr = nullptr, *w_lag = nullptr, *w_val = nullptr;
   int last_launches = 0;
   // tensor-core bank path (corr_tc.cuh)
+  bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
   bool tc = false;
   int tc_sms = 148;
   TcParams tcp{};
@@ -303,6 +304,13 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
     if (p->d_taps) { cudaFree(p->d_taps); p->d_taps = nullptr; }
     return cuda_status(e);
   }
+  // small tap tables travel in the SIMT correlation's kernel parameters (constant cache)
+  p->ctaps = false;
+  if ((int64_t)n_templates * p->taps_per_t <= kCTaps && !(std::getenv("SIDWT_CTAPS") && std::getenv("SIDWT_CTAPS")[0] == '0')) {
+    e = cudaMemcpy(p->cor.ctap, p->d_taps, tab_bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) { cudaFree(p->d_taps); p->d_taps = nullptr; return cuda_status(e); }
+    p->ctaps = true;
+  }
   configure_tc(p);
   if (p->tc) {
     const size_t img_bytes = (size_t)p->tcp.n_mt * p->tcp.total_ksteps * 8192;
@@ -446,11 +454,19 @@ static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t
   cudaError_t e;
   int minb = 3;                       // 3 CTAs x 8 warps per SM (measured best on C2)
   if (const char* ev = std::getenv("SIDWT_K2_MINB")) minb = std::max(1, std::min(4, atoi(ev)));
-  void (*kern)(const void*, const void*, void*, void*, CorParams);
-  if (is_int(p)) kern = minb <= 1 ? k_correlate<true, kQ, 1> : minb == 2 ? k_correlate<true, kQ, 2>
-                      : minb == 3 ? k_correlate<true, kQ, 3> : k_correlate<true, kQ, 4>;
-  else kern = minb <= 1 ? k_correlate<false, kQ, 1> : minb == 2 ? k_correlate<false, kQ, 2>
-              : minb == 3 ? k_correlate<false, kQ, 3> : k_correlate<false, kQ, 4>;
+  void (*kern)(const void*, const void*, void*, void*, const CorParams);
+  const bool ct = p->ctaps;
+  if (is_int(p)) {
+    if (ct) kern = minb <= 1 ? k_correlate<true, kQ, 1, true> : minb == 2 ? k_correlate<true, kQ, 2, true>
+                 : minb == 3 ? k_correlate<true, kQ, 3, true> : k_correlate<true, kQ, 4, true>;
+    else kern = minb <= 1 ? k_correlate<true, kQ, 1, false> : minb == 2 ? k_correlate<true, kQ, 2, false>
+              : minb == 3 ? k_correlate<true, kQ, 3, false> : k_correlate<true, kQ, 4, false>;
+  } else {
+    if (ct) kern = minb <= 1 ? k_correlate<false, kQ, 1, true> : minb == 2 ? k_correlate<false, kQ, 2, true>
+                 : minb == 3 ? k_correlate<false, kQ, 3, true> : k_correlate<false, kQ, 4, true>;
+    else kern = minb <= 1 ? k_correlate<false, kQ, 1, false> : minb == 2 ? k_correlate<false, kQ, 2, false>
+              : minb == 3 ? k_correlate<false, kQ, 3, false> : k_correlate<false, kQ, 4, false>;
+  }
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cor_smem);
   if (e == cudaSuccess) {
     kern<<<(unsigned)grid, kK2Threads, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
