@@ -426,6 +426,22 @@ __device__ __forceinline__ void corr_chunk(const typename std::conditional<INT, 
   else corr_chunk_f<Q, REM, true>(pr, plane, g, tp, wr, wi, ar, ai);
 }
 
+// Last chunk of an item: REM = rem taps (1..Q), dispatched to a compile-time length.
+template <bool INT, int Q, int R>
+__device__ __forceinline__ void corr_last(int rem, const typename std::conditional<INT, int, float>::type* pr, int plane, int g,
+                                          const typename std::conditional<INT, int2, float2>::type* tp,
+                                          typename std::conditional<INT, unsigned, float>::type (&wr)[Q],
+                                          typename std::conditional<INT, unsigned, float>::type (&wi)[Q],
+                                          typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
+                                          typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
+  if constexpr (R >= Q) {
+    corr_chunk<INT, Q, Q>(pr, plane, g, tp, wr, wi, ar, ai);
+  } else {
+    if (rem == R) corr_chunk<INT, Q, R>(pr, plane, g, tp, wr, wi, ar, ai);
+    else corr_last<INT, Q, R + 1>(rem, pr, plane, g, tp, wr, wi, ar, ai);
+  }
+}
+
 // One item: Q outputs q0..q0+Q-1 of residue r; band tile value for output q, tap k' at
 // sb[r + g (q + k')] (re plane) and sb[... + plane] (im plane).  No index clamps: the
 // tile holds every value the valid outputs need; outputs past the residue's end (the
@@ -453,23 +469,11 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
     if constexpr (INT) corr_chunk_i<Q, Q, false>(pr, plane, g, tp, wr, wi, ar, ai);
     else corr_chunk_f<Q, Q, false>(pr, plane, g, tp, wr, wi, ar, ai);
   }
-  switch (ntap - nfull * Q) {
-    case 1: corr_chunk<INT, Q, 1>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    case 2: corr_chunk<INT, Q, 2>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    case 3: corr_chunk<INT, Q, 3>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    case 4: corr_chunk<INT, Q, 4>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    case 5: corr_chunk<INT, Q, 5>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    case 6: corr_chunk<INT, Q, 6>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    case 7: corr_chunk<INT, Q, 7>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    case 8: corr_chunk<INT, Q, 8>(pr, plane, g, tp, wr, wi, ar, ai); break;
-    default: corr_chunk<INT, Q, Q>(pr, plane, g, tp, wr, wi, ar, ai); break;
-  }
+  corr_last<INT, Q, 1>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ar, ai);
 }
 
-// CT: the taps are read from the kernel parameters (uniform constant-cache loads, LDCU),
-// keeping the shared-memory pipe for the band values: per tap and item 2 LDS feed 4Q FFMA.
-template <bool INT, int Q, int MINB, bool CT>
-__global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
+template <bool INT, int Q, int NT, int MINB, bool CT>
+__global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
                                                    void* __restrict__ corr, void* __restrict__ partials,
                                                    const __grid_constant__ CorParams p) {
   typedef typename std::conditional<INT, int, float>::type T;
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(256, MINB) k_correlate(const void* __restrict_
   T2* stap = reinterpret_cast<T2*>(smem_raw + 16);
   T* sbuf = reinterpret_cast<T*>(smem_raw + 16 + (((size_t)p.taps_per_t * sizeof(T2) + 127) & ~(size_t)127));  // [2][2][balloc]
   T2* acc = reinterpret_cast<T2*>(sbuf + 2 * (size_t)p.nbuf * p.balloc);   // [2 buffers][TT] complex (re, im)
-  constexpr int kWarps = 256 / 32;
+  constexpr int kWarps = NT / 32;
   typedef typename std::conditional<INT, PeakI, PeakF>::type PK;
   __shared__ PK red[kMaxTerms][kWarps];
 

@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kRV = 15;     // K1 run length (odd: bank-conflict free)
 constexpr int kQ = 9;       // K2 outputs per item (odd: bank-conflict free)
-constexpr int kK2Threads = 256;
+constexpr int kK2NT = 256;  // K2 threads (Q = 11 with 192 threads measured slower on C2 and C5)
 
 inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -456,20 +456,17 @@ static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t
   if (const char* ev = std::getenv("SIDWT_K2_MINB")) minb = std::max(1, std::min(4, atoi(ev)));
   void (*kern)(const void*, const void*, void*, void*, const CorParams);
   const bool ct = p->ctaps;
+  const bool m3 = minb >= 3;
   if (is_int(p)) {
-    if (ct) kern = minb <= 1 ? k_correlate<true, kQ, 1, true> : minb == 2 ? k_correlate<true, kQ, 2, true>
-                 : minb == 3 ? k_correlate<true, kQ, 3, true> : k_correlate<true, kQ, 4, true>;
-    else kern = minb <= 1 ? k_correlate<true, kQ, 1, false> : minb == 2 ? k_correlate<true, kQ, 2, false>
-              : minb == 3 ? k_correlate<true, kQ, 3, false> : k_correlate<true, kQ, 4, false>;
+    if (ct) kern = m3 ? k_correlate<true, kQ, kK2NT, 3, true> : k_correlate<true, kQ, kK2NT, 2, true>;
+    else kern = m3 ? k_correlate<true, kQ, kK2NT, 3, false> : k_correlate<true, kQ, kK2NT, 2, false>;
   } else {
-    if (ct) kern = minb <= 1 ? k_correlate<false, kQ, 1, true> : minb == 2 ? k_correlate<false, kQ, 2, true>
-                 : minb == 3 ? k_correlate<false, kQ, 3, true> : k_correlate<false, kQ, 4, true>;
-    else kern = minb <= 1 ? k_correlate<false, kQ, 1, false> : minb == 2 ? k_correlate<false, kQ, 2, false>
-              : minb == 3 ? k_correlate<false, kQ, 3, false> : k_correlate<false, kQ, 4, false>;
+    if (ct) kern = m3 ? k_correlate<false, kQ, kK2NT, 3, true> : k_correlate<false, kQ, kK2NT, 2, true>;
+    else kern = m3 ? k_correlate<false, kQ, kK2NT, 3, false> : k_correlate<false, kQ, kK2NT, 2, false>;
   }
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->cor_smem);
   if (e == cudaSuccess) {
-    kern<<<(unsigned)grid, kK2Threads, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
+    kern<<<(unsigned)grid, kK2NT, p->cor_smem, s>>>(d_bands, p->d_taps, d_corr, p->d_partials, c);
     e = cudaGetLastError();
   }
   p->last_launches = 1;
