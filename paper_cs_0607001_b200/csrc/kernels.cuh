@@ -646,16 +646,27 @@ __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__
       }
     }
     if (p.want_peaks) {
+      if constexpr (INT) {
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        PK o;
-        o.m2 = __shfl_down_sync(0xffffffffu, best.m2, off);
-        o.tau = __shfl_down_sync(0xffffffffu, best.tau, off);
-        o.re = __shfl_down_sync(0xffffffffu, best.re, off);
-        o.im = __shfl_down_sync(0xffffffffu, best.im, off);
-        if (o.tau >= 0 && (best.tau < 0 || beats(o.m2, o.tau, best.m2, best.tau))) best = o;
+        for (int off = 16; off > 0; off >>= 1) {
+          PK o;
+          o.m2 = __shfl_down_sync(0xffffffffu, best.m2, off);
+          o.tau = __shfl_down_sync(0xffffffffu, best.tau, off);
+          o.re = __shfl_down_sync(0xffffffffu, best.re, off);
+          o.im = __shfl_down_sync(0xffffffffu, best.im, off);
+          if (o.tau >= 0 && (best.tau < 0 || beats(o.m2, o.tau, best.m2, best.tau))) best = o;
+        }
+        if ((threadIdx.x & 31) == 0) red[ti][threadIdx.x >> 5] = best;
+      } else {
+        // warp argmax by two hardware reductions: the largest |.|^2 (float bits of a
+        // non-negative float order like unsigned ints), then the smallest lag attaining it
+        const unsigned mb = best.tau >= 0 ? __float_as_uint(best.m2) : 0u;
+        const unsigned mmax = __reduce_max_sync(0xffffffffu, mb);
+        const unsigned cand = (best.tau >= 0 && mb == mmax) ? (unsigned)best.tau : 0xffffffffu;
+        const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
+        if (best.tau >= 0 && (unsigned)best.tau == tmin) red[ti][threadIdx.x >> 5] = best;
+        else if ((threadIdx.x & 31) == 0 && tmin == 0xffffffffu) { PK e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; red[ti][threadIdx.x >> 5] = e; }
       }
-      if ((threadIdx.x & 31) == 0) red[ti][threadIdx.x >> 5] = best;
     }
   }
   if (p.want_peaks) {
