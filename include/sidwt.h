@@ -141,6 +141,18 @@ sidwt_status sidwt_peaks(sidwt_plan plan, const void* d_corr, int64_t rows, int3
 sidwt_status sidwt_correlate_peaks(sidwt_plan plan, const void* d_bands, int64_t rows,
                                    void* d_corr, int32_t* d_lag, void* d_val, void* stream);
 
+/* Synthesis by inverse lifting (coarse to fine, eq. (21); the
+ * perfect-reconstruction property of the lifting factorisation, PAPER.md:61-63,
+ * 173-179): from bands produced by sidwt_analyze, rebuild the approximation band
+ * U_level (0 <= level < levels) at the fine-grid positions 0 .. N-1, using U_J and
+ * W_J .. W_{level+1} and the inverse of the received (dual analysis) lifting program.
+ * level 0 reconstructs the row itself (exactly, for SIDWT_LEGALL53_INT).
+ * d_out: device, [rows][N] complex64, or int32x2 for the integer family.
+ * Errors: DEPTH if level is outside [0, levels); STATE before template_load (the
+ * band layout is fixed there; its margins include the synthesis reach). */
+sidwt_status sidwt_synthesize(sidwt_plan plan, const void* d_bands, int64_t rows, int level,
+                              void* d_out, void* stream);
+
 /* End-to-end from HOST memory: copy rows host->device, analyze, correlate,
  * peaks, copy lag (and val if non-NULL) device->host, all on `stream`.
  * Uses plan-owned device buffers (allocated on first use for `batch` rows;

@@ -49,6 +49,7 @@ def lib():
         L.oracle_template_pyramid.argtypes = [i, i, i, P, P]
         L.oracle_run.argtypes = [i, i, i, i, i, P, i, i, P, i, i, P, P, P, P, i]
         L.oracle_max_threads.restype = i
+        L.oracle_approx.argtypes = [i, i, i, i, P, i, i, i, P, i]
         _lib = L
     return _lib
 
@@ -161,6 +162,27 @@ def run(family: int, J: int, ext: int, N: int, y: np.ndarray, x: np.ndarray,
     if rc != 0:
         raise ValueError("oracle_run rejected its arguments")
     return dict(bands=bands, corr=cr, lag=lag, val=val)
+
+
+def approx(family: int, ext: int, N: int, y: np.ndarray, s: int, p_lo: int = 0, p_hi: int | None = None,
+           nthreads: int = 0):
+    """Approximation band U_s of each row at positions [p_lo, p_hi) (default [0, N)):
+    complex128 [rows][n] (float families) or int64 [rows][n][2] (integer family)."""
+    isint = family == LEGALL53_INT
+    p_hi = N if p_hi is None else p_hi
+    if isint:
+        y = np.ascontiguousarray(y, dtype=np.int16)
+        if y.ndim == 2:
+            y = y[None]
+        out = np.zeros((y.shape[0], p_hi - p_lo, 2), np.int64)
+    else:
+        y = np.ascontiguousarray(y, dtype=np.complex128)
+        if y.ndim == 1:
+            y = y[None]
+        out = np.zeros((y.shape[0], p_hi - p_lo), np.complex128)
+    if lib().oracle_approx(family, ext, N, y.shape[0], _p(y), s, p_lo, p_hi, _p(out), nthreads) != 0:
+        raise ValueError("oracle_approx rejected its arguments")
+    return out
 
 
 def max_threads() -> int:

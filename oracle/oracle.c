@@ -519,6 +519,81 @@ static void run_row_int(int J, int ext, int N, const int16_t* y, int n_t, const 
     free(D);
 }
 
+/* Approximation band U_s (s = 0..J) of one row at fine-grid positions [p_lo, p_hi), by the
+ * same even/odd tree (O4) as oracle_run; U_0 is the extended row (O1).  Used to check the
+ * GPU synthesis (inverse lifting, eq. (21)) against the forward tree. */
+static void approx_row_float(int family, int ext, int N, const cplx* y, int s, int p_lo, int p_hi, cplx* out) {
+    filt_t lp;
+    get_filter(family, OR_DUAL, OR_LOWPASS, &lp);
+    int P = (ext == OR_PERIODIC) ? N : (N == 1 ? 1 : 2 * N - 2);
+    cplx* cur = (cplx*)malloc(sizeof(cplx) * P);
+    for (int n = 0; n < P; n++) cur[n] = y[ext_index(ext, N, n)];
+    for (int l = 1; l <= s; l++) {
+        int Po = out_period(P);
+        long nbr = 1L << (l - 1);
+        cplx* nxt = (cplx*)malloc(sizeof(cplx) * (size_t)(2 * nbr) * Po);
+        cplx* vplus = (cplx*)malloc(sizeof(cplx) * P);
+        for (long r = 0; r < nbr; r++) {
+            const cplx* v = cur + r * P;
+            mallat_periodic(&lp, v, P, nxt + r * Po);
+            for (int k = 0; k < P; k++) vplus[k] = v[imod(k + 1, P)];
+            mallat_periodic(&lp, vplus, P, nxt + (r + nbr) * Po);
+        }
+        free(vplus);
+        free(cur);
+        cur = nxt;
+        P = Po;
+    }
+    for (long p = p_lo; p < p_hi; p++) out[p - p_lo] = band_at(cur, s, P, p);
+    free(cur);
+}
+
+static void approx_row_int(int ext, int N, const int16_t* y, int s, int p_lo, int p_hi, int64_t* out) {
+    int P = (ext == OR_PERIODIC) ? N : (N == 1 ? 1 : 2 * N - 2);
+    for (int q = 0; q < 2; q++) {
+        int Pq = P;
+        int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * Pq);
+        for (int n = 0; n < Pq; n++) cur[n] = y[2 * ext_index(ext, N, n) + q];
+        for (int l = 1; l <= s; l++) {
+            int Po = out_period(Pq);
+            long nbr = 1L << (l - 1);
+            int64_t* nxt = (int64_t*)malloc(sizeof(int64_t) * (size_t)(2 * nbr) * Po);
+            int64_t* det = (int64_t*)malloc(sizeof(int64_t) * (size_t)Po);
+            int64_t* vplus = (int64_t*)malloc(sizeof(int64_t) * Pq);
+            for (long r = 0; r < nbr; r++) {
+                const int64_t* v = cur + r * Pq;
+                oracle_int_level(OR_DUAL, Pq, v, nxt + r * Po, det);
+                for (int k = 0; k < Pq; k++) vplus[k] = v[imod(k + 1, Pq)];
+                oracle_int_level(OR_DUAL, Pq, vplus, nxt + (r + nbr) * Po, det);
+            }
+            free(vplus);
+            free(det);
+            free(cur);
+            cur = nxt;
+            Pq = Po;
+        }
+        for (long p = p_lo; p < p_hi; p++) out[(p - p_lo) * 2 + q] = band_at_i(cur, s, Pq, p);
+        free(cur);
+    }
+}
+
+int oracle_approx(int family, int ext, int N, int rows, const void* y, int s, int p_lo, int p_hi, void* out,
+                  int nthreads) {
+    if (family < 0 || family > 3 || N < 2 || (N & (N - 1)) || s < 0 || (1L << s) > N) return -1;
+    if (ext != OR_PERIODIC && ext != OR_SYMMETRIC) return -1;
+    if (rows < 0 || p_hi <= p_lo) return -1;
+    long nb = p_hi - p_lo;
+    if (nthreads <= 0) nthreads = oracle_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+    for (int r = 0; r < rows; r++) {
+        if (family != OR_LEGALL53_INT)
+            approx_row_float(family, ext, N, (const cplx*)y + (long)r * N, s, p_lo, p_hi, (cplx*)out + (long)r * nb);
+        else
+            approx_row_int(ext, N, (const int16_t*)y + (long)r * N * 2, s, p_lo, p_hi, (int64_t*)out + (long)r * nb * 2);
+    }
+    return 0;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -65,6 +65,12 @@ int oracle_run(int family, int J, int ext, int N, int rows, const void* y,
                int T, int n_t, const void* x, int p_lo, int p_hi, void* bands,
                void* corr, int32_t* lag, void* val, int nthreads);
 
+/* Approximation band U_s (s >= 0; U_0 = the extended row) at fine-grid positions
+ * [p_lo, p_hi) of each row, by the tree of oracle_run.  out: [rows][p_hi - p_lo] complex
+ * double (int64 pairs for the integer family).  Returns 0 or -1. */
+int oracle_approx(int family, int ext, int N, int rows, const void* y, int s, int p_lo, int p_hi, void* out,
+                  int nthreads);
+
 int oracle_max_threads(void);
 
 #ifdef __cplusplus

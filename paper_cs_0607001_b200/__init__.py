@@ -136,6 +136,14 @@ class Plan:
         _native.sidwt_correlate_peaks(self.handle, bands, rows, corr, lag, val, self._stream(stream))
         return corr, lag, val
 
+    def synthesize(self, bands, rows: int, level: int = 0, out=None, stream=None):
+        """Inverse lifting: U_level at positions 0..N-1 ([rows][N][2] float32 / int32)."""
+        if out is None:
+            dt = self.torch.int32 if self.is_int else self.torch.float32
+            out = self.torch.empty((rows, self.N, 2), dtype=dt, device=self.device)
+        _native.sidwt_synthesize(self.handle, bands, rows, level, out, self._stream(stream))
+        return out
+
     def execute_host(self, h_rows, rows: int, h_lag, h_val=None, stream=None):
         _native.sidwt_execute_host(self.handle, h_rows, rows, h_lag, h_val, self._stream(stream))
 

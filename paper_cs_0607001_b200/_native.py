@@ -28,7 +28,7 @@ STATUS = {0: "SIDWT_OK", 1: "SIDWT_ERR_PARAM", 2: "SIDWT_ERR_LENGTH", 3: "SIDWT_
 
 # every symbol include/sidwt.h declares
 EXPORTS = ["sidwt_plan_create", "sidwt_plan_destroy", "sidwt_template_load", "sidwt_analyze",
-           "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_execute_host",
+           "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_synthesize", "sidwt_execute_host",
            "sidwt_band_stride", "sidwt_band_offset", "sidwt_bands_bytes", "sidwt_corr_bytes",
            "sidwt_template_taps", "sidwt_last_launches", "sidwt_uses_tensor_cores", "sidwt_status_string"]
 
@@ -71,6 +71,7 @@ def lib():
         L.sidwt_peaks.argtypes = [P, P, I64, P, P, P]
         L.sidwt_correlate_peaks.argtypes = [P, P, I64, P, P, P, P]
         L.sidwt_execute_host.argtypes = [P, P, I64, P, P, P]
+        L.sidwt_synthesize.argtypes = [P, P, I64, I, P, P]
         for f in ("sidwt_band_stride", "sidwt_band_offset"):
             getattr(L, f).argtypes = [P]
             getattr(L, f).restype = I64
@@ -146,6 +147,10 @@ def sidwt_peaks(plan, d_corr, rows, d_lag, d_val=None, stream=None):
 def sidwt_correlate_peaks(plan, d_bands, rows, d_corr, d_lag, d_val=None, stream=None):
     _check("sidwt_correlate_peaks", lib().sidwt_correlate_peaks(
         plan, _ptr(d_bands), rows, _ptr(d_corr), _ptr(d_lag), _ptr(d_val), _stream(stream)))
+
+
+def sidwt_synthesize(plan, d_bands, rows, level, d_out, stream=None):
+    _check("sidwt_synthesize", lib().sidwt_synthesize(plan, _ptr(d_bands), rows, level, _ptr(d_out), _stream(stream)))
 
 
 def sidwt_execute_host(plan, h_rows, rows, h_lag, h_val=None, stream=None):

@@ -311,6 +311,75 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
 }
 
 // ---------------------------------------------------------------------------
+// K4: synthesis (inverse lifting, eq. (21); PR property PAPER.md:61-63,
+// 173-179): U_level over fine-grid positions [0, N) from U_J and W_J .. W_{level+1},
+// coarse to fine.  One CTA per (row, component, tile of TL positions); the buffer holds
+// the tile plus the accumulated inverse reach; level l needs U_l, W_l at tau + 2h m.
+// ---------------------------------------------------------------------------
+struct SynParams {
+  int N, J, ext, stride, ML, level, TL, ntiles, halo_l, halo_r, lbuf;
+  long long rows;
+};
+
+template <int FAM>
+__global__ void __launch_bounds__(256) k_synthesize(const void* __restrict__ bands, void* __restrict__ out, SynParams p) {
+  typedef typename Inverse<FAM>::T T;
+  constexpr int SL = Inverse<FAM>::SL, SR = Inverse<FAM>::SR, W = SL + SR + 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* A = reinterpret_cast<T*>(smem_raw);
+  T* B = A + p.lbuf;
+  T* C = B + p.lbuf;
+  const int tile = blockIdx.x % p.ntiles;
+  const long long rc = blockIdx.x / p.ntiles;
+  const int comp = (int)(rc & 1);
+  const long long row = rc >> 1;
+  const int t0 = tile * p.TL;
+  const int P0 = t0 - p.halo_l;                                  // position of buffer index 0
+  const T* brow = static_cast<const T*>(bands) + (size_t)row * (p.J + 1) * 2 * p.stride + (size_t)comp * p.stride;
+  // stored index of fine-grid position pos of band `band` (b < J: W_{b+1}, b = J: U_J)
+  auto bidx = [&](int band, int pos) -> int {
+    if (p.ext == 0) return pos & (p.N - 1);
+    const int lo = -p.ML, hi = p.stride - p.ML;                  // stored positions [lo, hi)
+    if (pos >= lo && pos < hi) return pos + p.ML;
+    // symmetric families (host-guaranteed for 5/3, 9/7, int 5/3): period 2N-2, then
+    // reflection of U about 0 / of W_{b+1} about -2^b
+    const int P = 2 * p.N - 2;
+    int m = pos % P;
+    if (m < 0) m += P;
+    if (m < hi) return m + p.ML;
+    if (m - P >= lo) return m - P + p.ML;
+    int q = (band == p.J) ? P - m : -(2 << band) - m;
+    while (q < lo) q += P;
+    while (q >= hi) q -= P;
+    return q + p.ML;
+  };
+  auto load_band = [&](int band, T* dst) {
+    const T* src = brow + (size_t)band * 2 * p.stride;
+    for (int u = threadIdx.x; u < p.lbuf; u += blockDim.x) dst[u] = src[bidx(band, P0 + u)];
+  };
+  load_band(p.J, A);                                              // U_J
+  int lo = 0, hi = p.lbuf;                                        // valid range of A
+  for (int l = p.J; l > p.level; --l) {
+    const int st = 1 << l;                                        // pair step 2h, h = 2^{l-1}
+    load_band(l - 1, B);                                          // W_l
+    __syncthreads();
+    const int nlo = lo + SL * st, nhi = hi - SR * st;
+    for (int u = nlo + threadIdx.x; u < nhi; u += blockDim.x) {
+      T c[W], d[W];
+#pragma unroll
+      for (int m = 0; m < W; ++m) { c[m] = A[u + (m - SL) * st]; d[m] = B[u + (m - SL) * st]; }
+      C[u] = Inverse<FAM>::e(c, d);
+    }
+    __syncthreads();
+    T* tmp = A; A = C; C = tmp;
+    lo = nlo; hi = nhi;
+  }
+  const int n = min(p.TL, p.N - t0);
+  T* o = static_cast<T*>(out) + (size_t)row * p.N * 2 + comp;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) o[(size_t)(t0 + i) * 2] = A[p.halo_l + i];
+}
+
+// ---------------------------------------------------------------------------
 // Peak partial record (per row, template, scale, lag tile).
 // ---------------------------------------------------------------------------
 struct PeakF { float m2; int tau; float re, im; };

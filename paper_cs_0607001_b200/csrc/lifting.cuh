@@ -110,6 +110,80 @@ template <> struct Dual<FI53> {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Inverse dual-analysis programs (synthesis, eq. (21): the finer
+// approximation from the coarser (approximation, detail) pair by the inverse lifting
+// steps).  On the fine grid: U_{s-1}[tau] = e of the pair at tau, from c = U_s and
+// d = W_s at tau + 2h m (h = 2^{s-1}); c[i], d[i] hold m = i - SL.
+// ---------------------------------------------------------------------------
+template <int FAM> struct Inverse;
+
+// 5/3: o_k = d_k / 2 + (c_k + c_{k+1}) / 4 ; e_k = c_k - (o_k + o_{k-1}) / 2
+template <> struct Inverse<F53> {
+  typedef float T;
+  static constexpr int SL = 1, SR = 1;
+  __device__ __forceinline__ static float e(const float (&c)[3], const float (&d)[3]) {
+    const float ok = fmaf(0.5f, d[1], 0.25f * (c[1] + c[2]));
+    const float om = fmaf(0.5f, d[0], 0.25f * (c[0] + c[1]));
+    return fmaf(-0.5f, ok + om, c[1]);
+  }
+};
+
+// CDF 9/7 (reading R-D3): e4 = zeta c, o4 = d / zeta; o3 = o4 + delta (e4_k + e4_{k+1});
+// e2 = e4 + gamma (o3_k + o3_{k-1}); o1 = o3 + beta (e2_k + e2_{k+1}); e = e2 + alpha (o1_k + o1_{k-1})
+template <> struct Inverse<F97> {
+  typedef float T;
+  static constexpr int SL = 2, SR = 2;
+  __device__ __forceinline__ static float e(const float (&c)[5], const float (&d)[5]) {
+    const float z = (float)kZeta, iz = (float)(1.0 / kZeta);
+    float e4[5], o4[4], o3[4], e2[3], o1[2];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) e4[i] = z * c[i];          // m = i - 2
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o4[i] = iz * d[i];         // m = i - 2
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o3[i] = fmaf((float)kDelta, e4[i] + e4[i + 1], o4[i]);   // m = i - 2
+#pragma unroll
+    for (int i = 0; i < 3; ++i) e2[i] = fmaf((float)kGamma, o3[i + 1] + o3[i], e4[i + 1]);  // m = i - 1
+#pragma unroll
+    for (int i = 0; i < 2; ++i) o1[i] = fmaf((float)kBeta, e2[i] + e2[i + 1], o3[i + 1]);   // m = i - 1
+    return fmaf((float)kAlpha, o1[1] + o1[0], e2[1]);
+  }
+};
+
+// causal D4 (eq. (17), reading R-D1): e1 = c / K1, o2 = d / K2, o1_k = o2_{k+1} - e1_{k+1},
+// e_k = e1_k - c1 o1_k - c2 o1_{k-1} with o1_{k-1} = o2_k - e1_k
+template <> struct Inverse<FD4> {
+  typedef float T;
+  static constexpr int SL = 0, SR = 1;
+  __device__ __forceinline__ static float e(const float (&c)[2], const float (&d)[2]) {
+    const float ik1 = (float)(1.0 / kD4K1), ik2 = (float)(1.0 / kD4K2);
+    const float e1k = ik1 * c[0], e1n = ik1 * c[1];
+    const float o1k = fmaf(ik2, d[1], -e1n), o1m = fmaf(ik2, d[0], -e1k);
+    return fmaf(-(float)kD4c2, o1m, fmaf(-(float)kD4c1, o1k, e1k));
+  }
+};
+
+// reversible integer 5/3 (reading R-INT): o_k = d_k + ((c_k + c_{k+1} + 2) >> 2);
+// e_k = c_k - ((o_k + o_{k-1}) >> 1)  -- the exact inverse of the received program
+template <> struct Inverse<FI53> {
+  typedef int T;
+  static constexpr int SL = 1, SR = 1;
+  __device__ __forceinline__ static int e(const int (&c)[3], const int (&d)[3]) {
+    const int ok = d[1] + ((c[1] + c[2] + 2) >> 2);
+    const int om = d[0] + ((c[0] + c[1] + 2) >> 2);
+    return c[1] - ((ok + om) >> 1);
+  }
+};
+
+__host__ __device__ inline void inverse_reach(int fam, int& sl, int& sr) {
+  switch (fam) {
+    case F97: sl = 2; sr = 2; break;
+    case FD4: sl = 0; sr = 1; break;
+    default:  sl = 1; sr = 1; break;
+  }
+}
+
 // Reach of one level in units of the level stride h = 2^{s-1}: the approximation at
 // tau reads U over [tau - lowL h, tau + lowR h]; the detail over [tau - hiL h, tau + hiR h].
 struct Reach { int lowL, lowR, hiL, hiR; };

@@ -151,6 +151,19 @@ static void configure(sidwt_plan_s* p) {
     ML = std::max(ML, -g * p->kmin[i]);
     MR = std::max(MR, g * (p->kmin[i] + p->cnt[i] - 1));
   }
+  // synthesis (sidwt_synthesize): 5/3, 9/7 and integer 5/3 bands of a symmetric extension
+  // are (2N-2)-periodic and whole-sample symmetric (U_s about 0, W_s about -2^{s-1};
+  // SURVEY App. A.4), so out-of-range reads reflect into the stored range once it covers
+  // (-2^J, 0); causal D4 bands have no symmetry and the margin holds the inverse reach.
+  if (p->fam == FD4) {
+    int sl = 0, sr = 0;
+    inverse_reach(p->fam, sl, sr);
+    const int span = (1 << (J + 1)) - 2;                         // sum_{l=1..J} 2^l
+    ML = std::max(ML, sl * span);
+    MR = std::max(MR, sr * span);
+  } else {
+    ML = std::max(ML, 1 << J);
+  }
   if (p->ext == SIDWT_EXT_PERIODIC) { ML = 0; MR = 0; }
   p->ML = ML; p->MR = MR;
   p->stride = rup(ML + p->N + MR, 32);
@@ -509,6 +522,47 @@ sidwt_status sidwt_peaks(sidwt_plan p, const void* d_corr, int64_t rows, int32_t
   else k_peaks<false><<<(unsigned)count, 256, 0, s>>>(d_corr, (int)p->N, d_lag, d_val);
   p->last_launches = 1;
   return cuda_status(cudaGetLastError());
+}
+
+template <int FAM>
+static cudaError_t launch_synthesize(const sidwt_plan_s* p, const void* bands, int64_t rows, int level, void* out,
+                                     cudaStream_t s) {
+  int sl = 0, sr = 0;
+  inverse_reach(p->fam, sl, sr);
+  SynParams q{};
+  q.N = (int)p->N; q.J = p->J; q.ext = p->ext; q.stride = (int)p->stride; q.ML = p->ML; q.level = level;
+  q.TL = (int)std::min<int64_t>(p->N, 2048);
+  q.ntiles = (int)cdiv(p->N, q.TL);
+  const int span = (1 << (p->J + 1)) - (1 << (level + 1));
+  q.halo_l = sl * span; q.halo_r = sr * span;
+  q.lbuf = (int)rup(q.halo_l + q.TL + q.halo_r, 4);
+  q.rows = rows;
+  const size_t smem = (size_t)3 * q.lbuf * 4;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  auto kern = k_synthesize<FAM>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)(rows * 2 * q.ntiles), 256, smem, s>>>(bands, out, q);
+  return cudaGetLastError();
+}
+
+sidwt_status sidwt_synthesize(sidwt_plan p, const void* d_bands, int64_t rows, int level, void* d_out, void* stream) {
+  if (!p || !d_bands || !d_out) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  if (level < 0 || level >= p->J) return SIDWT_ERR_DEPTH;
+  if (rows * 2 * cdiv(p->N, 2048) > 0x7fffffffLL) return SIDWT_ERR_RANGE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (p->fam) {
+    case F53: e = launch_synthesize<F53>(p, d_bands, rows, level, d_out, s); break;
+    case F97: e = launch_synthesize<F97>(p, d_bands, rows, level, d_out, s); break;
+    case FD4: e = launch_synthesize<FD4>(p, d_bands, rows, level, d_out, s); break;
+    default:  e = launch_synthesize<FI53>(p, d_bands, rows, level, d_out, s); break;
+  }
+  p->last_launches = 1;
+  if (e == cudaErrorInvalidValue) { cudaGetLastError(); return SIDWT_ERR_RANGE; }
+  return cuda_status(e);
 }
 
 sidwt_status sidwt_execute_host(sidwt_plan p, const void* h_rows, int64_t rows, int32_t* h_lag, void* h_val,

@@ -501,3 +501,51 @@ def test_int53_close_to_exact_correlation():
     ci = ri["corr"][0, 0, 0, :, 0] + 1j * ri["corr"][0, 0, 0, :, 1]
     assert np.abs(ci - ref).max() < 1e-3 * np.abs(ref).max()
     assert ri["lag"][0, 0, 0] == truth[0][1]
+
+
+# ---------------------------------------------------------------- approximation bands (synthesis checks)
+
+@pytest.mark.parametrize("fam", FAMS_FLOAT)
+@pytest.mark.parametrize("ext", (O.PERIODIC, O.SYMMETRIC))
+def test_approx_bands_are_a_trous_lowpass(fam, ext):
+    """oracle.approx (the forward tree's U_s, used to check the GPU synthesis of eq. (21),
+    PAPER.md:296-298): U_0 is the extended row (O1), U_J equals oracle_run's band J, and every
+    level is the undecimated lowpass U_s[tau] = sum_m f[m] U_{s-1}[tau - 2^{s-1} m] (R-D5)."""
+    N, J = 32, 3
+    y = RNG.normal(size=N) + 1j * RNG.normal(size=N)
+    p_lo, p_hi = -40, N + 70
+    lo_l, fl = O.filt(fam, O.DUAL, O.LOWPASS)
+    span = 400
+    pos = np.arange(-span, span + 1)
+    U = _extend(y, ext, pos)
+    sel = slice(p_lo + span, p_hi + span)
+    np.testing.assert_allclose(O.approx(fam, ext, N, y[None], 0, p_lo, p_hi)[0], U[sel], atol=0)
+    for s in range(1, J + 1):
+        h = 2 ** (s - 1)
+        Un = np.zeros_like(U)
+        for i, m in enumerate(range(lo_l, lo_l + len(fl))):
+            Un += fl[i] * np.roll(U, h * m)
+        U = Un
+        np.testing.assert_allclose(O.approx(fam, ext, N, y[None], s, p_lo, p_hi)[0], U[sel], atol=1e-12)
+    r = O.run(fam, J, ext, N, y[None], np.ones((1, 2)), p_lo=p_lo, p_hi=p_hi, corr=False)
+    np.testing.assert_allclose(O.approx(fam, ext, N, y[None], J, p_lo, p_hi)[0], r["bands"][0, J], atol=0)
+
+
+@pytest.mark.parametrize("ext", (O.PERIODIC, O.SYMMETRIC))
+def test_approx_bands_integer(ext):
+    """Integer family: U_0 is the extended I/Q row exactly; U_J equals oracle_run's band J."""
+    N, J = 64, 4
+    y = RNG.integers(-3000, 3000, size=(1, N, 2)).astype(np.int16)
+    p_lo, p_hi = -20, N + 30
+    u0 = O.approx(O.LEGALL53_INT, ext, N, y, 0, p_lo, p_hi)[0]
+    idx = np.array([_ext_index(ext, N, p) for p in range(p_lo, p_hi)])
+    assert np.array_equal(u0, y[0][idx].astype(np.int64))
+    r = O.run(O.LEGALL53_INT, J, ext, N, y, np.ones((1, 2, 2), np.int16), p_lo=p_lo, p_hi=p_hi, corr=False)
+    assert np.array_equal(O.approx(O.LEGALL53_INT, ext, N, y, J, p_lo, p_hi)[0], r["bands"][0, J])
+
+
+def _ext_index(ext, N, n):
+    if ext == O.PERIODIC:
+        return n % N
+    m = n % (2 * N - 2)
+    return m if m < N else 2 * N - 2 - m
