@@ -751,22 +751,37 @@ __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__
   }
 }
 
-// Combine per-tile peak partials (tiles ordered by lag: ties keep the earlier tile).
+// Combine per-tile peak partials (tiles ordered by lag: ties keep the earlier tile; the
+// comparison carries the lag, so the combination order does not matter).  One warp per
+// (row, template, scale): coalesced reads of its partials, shuffle reduction.
 template <bool INT>
-__global__ void k_peaks_finalize(const void* __restrict__ partials, int ntiles, long long count,
-                                 int32_t* __restrict__ lag, void* __restrict__ val) {
+__global__ void __launch_bounds__(256) k_peaks_finalize(const void* __restrict__ partials, int ntiles, long long count,
+                                                        int32_t* __restrict__ lag, void* __restrict__ val) {
   typedef typename std::conditional<INT, PeakI, PeakF>::type PK;
   typedef typename std::conditional<INT, int2, float2>::type T2;
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= count) return;
   const PK* pp = static_cast<const PK*>(partials) + (size_t)i * ntiles;
-  PK b = pp[0];
-  for (int k = 1; k < ntiles; ++k) {
+  PK b;
+  b.m2 = 0; b.tau = -1; b.re = 0; b.im = 0;
+  for (int k = lane; k < ntiles; k += 32) {
     const PK o = pp[k];
-    if (beats(o.m2, o.tau, b.m2, b.tau)) b = o;
+    if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
   }
-  lag[i] = b.tau;
-  if (val) { T2 v; v.x = b.re; v.y = b.im; static_cast<T2*>(val)[i] = v; }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    PK o;
+    o.m2 = __shfl_down_sync(0xffffffffu, b.m2, off);
+    o.tau = __shfl_down_sync(0xffffffffu, b.tau, off);
+    o.re = __shfl_down_sync(0xffffffffu, b.re, off);
+    o.im = __shfl_down_sync(0xffffffffu, b.im, off);
+    if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
+  }
+  if (lane == 0) {
+    lag[i] = b.tau;
+    if (val) { T2 v; v.x = b.re; v.y = b.im; static_cast<T2*>(val)[i] = v; }
+  }
 }
 
 // K3: standalone peak search over a stored correlation [count][N].

@@ -448,7 +448,7 @@ static sidwt_status correlate_tc(sidwt_plan_s* p, const void* d_bands, int64_t r
   p->last_launches = 1;
   if (e == cudaSuccess && peaks) {
     const int64_t count = rows * p->n_t * (p->J + 1);
-    k_peaks_finalize<false><<<(unsigned)cdiv(count, 256), 256, 0, s>>>(p->d_partials, 2 * t.ntiles, count, d_lag, d_val);
+    k_peaks_finalize<false><<<(unsigned)cdiv(count, 8), 256, 0, s>>>(p->d_partials, 2 * t.ntiles, count, d_lag, d_val);
     e = cudaGetLastError();
     p->last_launches = 2;
   }
@@ -485,7 +485,7 @@ static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t
   p->last_launches = 1;
   if (e == cudaSuccess && peaks) {
     const int64_t count = rows * p->n_t * (p->J + 1);
-    const unsigned blocks = (unsigned)cdiv(count, 256);
+    const unsigned blocks = (unsigned)cdiv(count, 8);           // one warp per (row, template, scale)
     if (is_int(p)) k_peaks_finalize<true><<<blocks, 256, 0, s>>>(p->d_partials, c.ntiles, count, d_lag, d_val);
     else k_peaks_finalize<false><<<blocks, 256, 0, s>>>(p->d_partials, c.ntiles, count, d_lag, d_val);
     e = cudaGetLastError();

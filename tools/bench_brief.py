@@ -8,6 +8,6 @@ s = d.get("stages", {})
 a, c = s.get("analyze", {}), s.get("correlate_peaks", {})
 print(sys.argv[1].split("/")[-1], "| %.3g samples/s" % d["value"], "| ms/step %.3f" % d["ms_per_step"],
       "| analyze %.3f ms %.0f GB/s (%.0f%%)" % (a.get("ms", 0), a.get("achieved", 0), 100 * a.get("frac", 0)),
-      "| corr %.3f ms %.1f TF" % (c.get("ms", 0), c.get("alu", {}).get("achieved", 0)),
+      "| corr %.3f ms %.1f TF" % (c.get("ms", 0), (c.get("alu") or c.get("tensor") or {}).get("achieved", 0)),
       "| e2e %s" % (d.get("e2e", {}) or {}).get("value"), "| cpu %s" % (d.get("cpu_baseline", {}) or {}).get("value"),
       "| clocks", d.get("clocks"))

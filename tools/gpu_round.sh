@@ -16,3 +16,9 @@ timeout 300 $CMD > $OUT/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_analyze|k_correlate" -s 4 -c 2 -o $OUT/prof_$TAG $CMD > $OUT/ncu_full_$TAG.log 2>&1
 echo "ncu rc=$?"
+# tensor-core bank kernel: launch list share and one full capture on a reduced C4 batch
+CMD4="python bench.py --config 4 --rows 256 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 300 $CMD4 > $OUT/plain4_$TAG.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches4_$TAG.csv $CMD4 > $OUT/ncu_launch4_$TAG.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_correlate_tc|k_analyze" -s 2 -c 2 -o $OUT/prof4_$TAG $CMD4 > $OUT/ncu_full4_$TAG.log 2>&1
+echo "ncu4 rc=$?"
