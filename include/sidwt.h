@@ -154,9 +154,11 @@ sidwt_status sidwt_synthesize(sidwt_plan plan, const void* d_bands, int64_t rows
                               void* d_out, void* stream);
 
 /* End-to-end from HOST memory: copy rows host->device, analyze, correlate,
- * peaks, copy lag (and val if non-NULL) device->host, all on `stream`.
+ * peaks, copy lag (and val if non-NULL) device->host, ordered on `stream`.
+ * Internally pipelined over row chunks on two plan-owned streams (the copy of
+ * chunk k overlaps the computation of chunk k-1), joined to `stream` by events.
  * Uses plan-owned device buffers (allocated on first use for `batch` rows;
- * SIDWT_ERR_OOM if they do not fit).  h_rows should be pinned for overlap.
+ * SIDWT_ERR_OOM if they do not fit).  h_rows must be pinned for the overlap.
  * Returns after enqueueing; synchronise `stream` before reading h_lag/h_val. */
 sidwt_status sidwt_execute_host(sidwt_plan plan, const void* h_rows, int64_t rows,
                                 int32_t* h_lag, void* h_val, void* stream);

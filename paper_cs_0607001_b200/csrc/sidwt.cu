@@ -24,6 +24,8 @@ constexpr int kRV = 15;     // K1 run length (odd: bank-conflict free)
 constexpr int kQ = 9;       // K2 outputs per item (odd: bank-conflict free)
 constexpr int kK2NT = 256;  // K2 threads (Q = 11 with 192 threads measured slower on C2 and C5)
 
+constexpr int kPipeChunks = 8;   // execute_host: host->device copy of chunk k overlaps compute of chunk k-1
+
 inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -51,6 +53,9 @@ struct sidwt_plan_s {
   void* d_partials = nullptr;
   size_t partials_bytes = 0;
   void *w_rows = nullptr, *w_bands = nullptr, *w_corr = nullptr, *w_lag = nullptr, *w_val = nullptr;
+  // execute_host pipeline
+  cudaStream_t s_copy = nullptr, s_comp = nullptr;
+  cudaEvent_t ev[10] = {};
   int last_launches = 0;
   // tensor-core bank path (corr_tc.cuh)
   bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
@@ -99,6 +104,9 @@ sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t 
 static void free_ws(sidwt_plan_s* p) {
   void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val, &p->d_img};
   for (void** b : bufs) { if (*b) cudaFree(*b); *b = nullptr; }
+  for (cudaEvent_t& ev : p->ev) { if (ev) cudaEventDestroy(ev); ev = nullptr; }
+  if (p->s_copy) { cudaStreamDestroy(p->s_copy); p->s_copy = nullptr; }
+  if (p->s_comp) { cudaStreamDestroy(p->s_comp); p->s_comp = nullptr; }
   p->partials_bytes = 0;
 }
 
@@ -565,6 +573,10 @@ sidwt_status sidwt_synthesize(sidwt_plan p, const void* d_bands, int64_t rows, i
   return cuda_status(e);
 }
 
+// End to end from host buffers, pipelined: the rows are cut into chunks; chunk k's
+// host->device copy (copy stream) overlaps the analyze + correlate + peaks of chunk k-1
+// (compute stream); both streams are ordered after, and the caller's stream after them,
+// by events, so the call is still stream-ordered on `stream`.
 sidwt_status sidwt_execute_host(sidwt_plan p, const void* h_rows, int64_t rows, int32_t* h_lag, void* h_val,
                                 void* stream) {
   if (!p || !h_rows || !h_lag) return SIDWT_ERR_PARAM;
@@ -577,18 +589,51 @@ sidwt_status sidwt_execute_host(sidwt_plan p, const void* h_rows, int64_t rows, 
   if (e == cudaSuccess && !p->w_corr) e = cudaMalloc(&p->w_corr, (size_t)sidwt_corr_bytes(p, p->batch));
   if (e == cudaSuccess && !p->w_lag) e = cudaMalloc(&p->w_lag, cnt * 4);
   if (e == cudaSuccess && !p->w_val) e = cudaMalloc(&p->w_val, cnt * 8);
+  if (e == cudaSuccess && !p->s_copy) e = cudaStreamCreateWithFlags(&p->s_copy, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !p->s_comp) e = cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking);
+  for (int k = 0; e == cudaSuccess && k < kPipeChunks + 2; ++k)
+    if (!p->ev[k]) e = cudaEventCreateWithFlags(&p->ev[k], cudaEventDisableTiming);
   if (e != cudaSuccess) return cuda_status(e);
+  sidwt_status st = ensure_partials(p);
+  if (st != SIDWT_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  e = cudaMemcpyAsync(p->w_rows, h_rows, (size_t)rows * p->N * sample_bytes(p), cudaMemcpyHostToDevice, s);
+  cudaEvent_t ev_start = p->ev[kPipeChunks], ev_done = p->ev[kPipeChunks + 1];
+  e = cudaEventRecord(ev_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_copy, ev_start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_comp, ev_start, 0);
   if (e != cudaSuccess) return cuda_status(e);
-  sidwt_status st = sidwt_analyze(p, p->w_rows, rows, p->w_bands, stream);
-  if (st != SIDWT_OK) return st;
-  st = sidwt_correlate_peaks(p, p->w_bands, rows, p->w_corr, static_cast<int32_t*>(p->w_lag), p->w_val, stream);
-  if (st != SIDWT_OK) return st;
-  const size_t n = (size_t)rows * p->n_t * (p->J + 1);
-  e = cudaMemcpyAsync(h_lag, p->w_lag, n * 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && h_val) e = cudaMemcpyAsync(h_val, p->w_val, n * 8, cudaMemcpyDeviceToHost, s);
-  p->last_launches = 3;
+  const int nch = (int)std::min<int64_t>(kPipeChunks, rows);
+  const int64_t per = cdiv(rows, nch);
+  const size_t sb = sample_bytes(p);
+  const size_t per_row_out = (size_t)p->n_t * (p->J + 1);
+  int launches = 0;
+  for (int k = 0; k < nch; ++k) {
+    const int64_t r0 = k * per, nr = std::min<int64_t>(per, rows - r0);
+    if (nr <= 0) break;
+    char* drows = static_cast<char*>(p->w_rows) + (size_t)r0 * p->N * sb;
+    e = cudaMemcpyAsync(drows, static_cast<const char*>(h_rows) + (size_t)r0 * p->N * sb, (size_t)nr * p->N * sb,
+                        cudaMemcpyHostToDevice, p->s_copy);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev[k], p->s_copy);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_comp, p->ev[k], 0);
+    if (e != cudaSuccess) return cuda_status(e);
+    char* dbands = static_cast<char*>(p->w_bands) + (size_t)sidwt_bands_bytes(p, r0);
+    char* dcorr = static_cast<char*>(p->w_corr) + (size_t)sidwt_corr_bytes(p, r0);
+    int32_t* dlag = static_cast<int32_t*>(p->w_lag) + r0 * per_row_out;
+    char* dval = static_cast<char*>(p->w_val) + (size_t)r0 * per_row_out * 8;
+    st = sidwt_analyze(p, drows, nr, dbands, p->s_comp);
+    if (st != SIDWT_OK) return st;
+    launches += p->last_launches;
+    st = sidwt_correlate_peaks(p, dbands, nr, dcorr, dlag, dval, p->s_comp);
+    if (st != SIDWT_OK) return st;
+    launches += p->last_launches;
+    e = cudaMemcpyAsync(h_lag + r0 * per_row_out, dlag, (size_t)nr * per_row_out * 4, cudaMemcpyDeviceToHost, p->s_comp);
+    if (e == cudaSuccess && h_val)
+      e = cudaMemcpyAsync(static_cast<char*>(h_val) + (size_t)r0 * per_row_out * 8, dval, (size_t)nr * per_row_out * 8,
+                          cudaMemcpyDeviceToHost, p->s_comp);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  e = cudaEventRecord(ev_done, p->s_comp);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_done, 0);
+  p->last_launches = launches;
   return cuda_status(e);
 }
-
