@@ -144,6 +144,11 @@ __device__ __forceinline__ void split_bf16(float v, float& hi, float& lo) {
 // Template operand images: img[mt][kstep][split][4096 B], K-major no-swizzle core
 // matrices: element (m, kk) at (m/8)*256 + (kk/8)*128 + (m%8)*16 + (kk%8)*2.
 // One thread per (mt, kstep, split, m).
+// Row order (TMEM lane of the accumulator): m = 32 q + 16 k + 8 c + b holds component c
+// (0 re, 1 im) of template tc_row_template(q, k, b) = 16 q + 8 k + (b >> 1) + 4 (b & 1), so a
+// 16x256b TMEM load gives each epilogue thread (re, im) of one template for two adjacent
+// lags, and the template rows of a quarter-warp differ in bit 2 (conflict-free swizzled
+// staging stores).
 // ---------------------------------------------------------------------------
 __global__ void k_tc_images(const float2* __restrict__ taps, int taps_per_t, TcParams p, unsigned char* __restrict__ img) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -160,8 +165,8 @@ __global__ void k_tc_images(const float2* __restrict__ taps, int taps_per_t, TcP
   const int kb_per_plane = tm.kp / 16;
   const int plane = kk / kb_per_plane;
   const int k0 = 16 * (kk % kb_per_plane);
-  const int t = mt * kTcTemplates + (m >> 1);
-  const int c = m & 1;
+  const int b = m & 7, c = (m >> 3) & 1, kq = m >> 4;             // kq = 2 q + k
+  const int t = mt * kTcTemplates + 8 * kq + (b >> 1) + 4 * (b & 1);
   unsigned char* blk = img + ((size_t)(mt * p.total_ksteps + q) * 2 + split) * 4096;
   for (int e = 0; e < 16; ++e) {
     const int kpp = k0 + e;
@@ -275,6 +280,18 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[3
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+// 16 lanes x 32 columns: thread t = a + 4 b gets, for rep r = 0..3, lanes b and b + 8 at
+// columns 8 r + 2 a, 8 r + 2 a + 1 -> registers 4 r + {0: (b, 2a), 1: (b, 2a+1), 2: (b+8, 2a), 3: (b+8, 2a+1)}
+__device__ __forceinline__ void tmem_ld16x256_x4(uint32_t taddr, uint32_t (&r)[32], int o) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[o + 0]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3]), "=r"(r[o + 4]), "=r"(r[o + 5]),
+        "=r"(r[o + 6]), "=r"(r[o + 7]), "=r"(r[o + 8]), "=r"(r[o + 9]), "=r"(r[o + 10]), "=r"(r[o + 11]),
+        "=r"(r[o + 12]), "=r"(r[o + 13]), "=r"(r[o + 14]), "=r"(r[o + 15])
+      : "r"(taddr));
+}
+
 // wait for this thread's outstanding tcgen05.ld; the registers of `r` are tied to the
 // wait so no use of them can be scheduled before it
 __device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
@@ -551,130 +568,118 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
              TC_CLOCK() - t_start, w_stg, w_ze, b_conv);
   } else {
     // ===================== epilogue (8 warps; TMEM lane group = warp & 3) =====================
-    // Lane pair (2 r, 2 r + 1) holds re / im of template row r for 32 lags per chunk.  One
-    // shuffle exchange gives each lane 16 complex values in "slots": even lane slot i =
-    // lag i, odd lane slot i = lag 16 + (i ^ 8).  They go to a per-warp staging area (two
-    // buffers, alternating per chunk) of two TMA boxes (lags 0-15 / 16-31) of 16 template
-    // rows x 128 B, 128B-swizzled: chunk q of row r at (q ^ (r & 7)); the slot rotation
-    // makes every quarter-warp's 16-byte stores hit 8 distinct bank groups.  A 4-D TMA
-    // tensor store per box writes corr (coalesced 128-byte rows, out-of-range templates
-    // clipped).  Peaks: |.|^2 max per chunk from the registers; the value at the winning
-    // lag is read back from the staging buffer.
+    // Per 32-lag chunk, two 16x256b TMEM loads (lane blocks k = 0, 1 of the warp's 32 lanes)
+    // give thread (a, b) the complex values of templates tr[k] = 8 k + (b >> 1) + 4 (b & 1)
+    // (of the warp's 16) at lags 8 rep + 2 a + {0, 1}, rep = 0..3: 16-byte (re, im, re, im)
+    // pairs, stored into a per-warp staging area (two buffers alternating per 32 lags; two
+    // TMA boxes lags 0-15 / 16-31 of 16 template rows x 128 B, 128B-swizzled: chunk q of row
+    // r at q ^ (r & 7); conflict-free), then a 4-D TMA tensor store per box (coalesced
+    // 128-byte rows; templates past n_t clipped by the tensor bounds).  Peaks from registers.
     const int ew = warp - kTcFirstEpi;
     const int lg = warp & 3;
     const int hh = ew >> 2;                                     // column half: chunks 4 hh .. 4 hh + 3
     unsigned char* epi = smem_raw + L.epi + ew * kTcEpiBytes;
-    const int r = lane >> 1;                                    // template row of this lane pair
-    const bool odd = lane & 1;
-    const int woff = (odd ? 2048 : 0) + r * 128;
-    const int sw = (r & 7) ^ (odd ? 4 : 0);                     // chunk q -> physical q ^ sw
-    long long w_acc = 0, t_start = TC_CLOCK(), e_bw = 0, e_ld = 0, e_st = 0;
+    const int ta = lane & 3, tb = lane >> 2;
+    const int tr0 = (tb >> 1) + 4 * (tb & 1), tr1 = 8 + tr0;     // template rows (of the warp's 16)
+    long long w_acc = 0, t_start = TC_CLOCK();
     long long u = 0;
+    int cb = 0;                                                 // staging buffer of the next chunk
     for (int pair = blockIdx.x; pair < (int)p.npairs; pair += gridDim.x) {
       for (int k = 0; k < units_per_pair; ++k, ++u) {
         const TcUnit un = tc_unit(p, pair, k);
         const int a = k & 1;
         const int ti = p.J - un.step;
         const int t0 = un.mt * kTcTemplates + lg * 16;
-        const bool valid = t0 + r < p.n_t;
         const int tau_h = un.tile * 256 + hh * 128;
         TC_TWAIT(&accfull[a], (uint32_t)((u >> 1) & 1), w_acc);
         tc_fence_after();
-        if (p.prof & 2) {                                       // debug: skip the epilogue work
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&accempty[a]);
-          continue;
-        }
-        float bm2 = -1.f, bre = 0.f, bim = 0.f;
-        int btau = 0x7fffffff;
+        float bm2[2] = {-1.f, -1.f}, bre[2] = {0.f, 0.f}, bim[2] = {0.f, 0.f};
+        int btau[2] = {0x7fffffff, 0x7fffffff};
         const uint32_t tcol = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * 256 + hh * 128);
 #pragma unroll 1
-        for (int c2 = 0; c2 < 2; ++c2) {
-          // two 32-lag chunks per staging fill: one proxy fence and one TMA group per 64 lags
-          const long long _e1 = TC_CLOCK();
-          if (lane == 0) bulk_wait_read_all();                  // previous group has read the staging
+        for (int c = 0; c < 4; ++c, cb ^= 1) {
+          uint32_t v[32];
+          tmem_ld16x256_x4(tcol + c * 32, v, 0);
+          tmem_ld16x256_x4(tcol + (16u << 16) + c * 32, v, 16);
+          tmem_wait_ld(v);
+          if (c == 3) {                                         // accumulator fully read: release it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[a]);
+          }
+          unsigned char* buf = epi + cb * 4096;
+          const int tau_c = tau_h + c * 32;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");   // buffer cb free
           __syncwarp();
-          e_bw += TC_CLOCK() - _e1;
-#pragma unroll 1
-          for (int h = 0; h < 2; ++h) {
-            const int c = 2 * c2 + h;
-            uint32_t v[32];
-            const long long _e0 = TC_CLOCK();
-            tmem_ld32_nowait(tcol + c * 32, v);
-            tmem_wait_ld(v);
-            e_ld += TC_CLOCK() - _e0;
-            if (c == 3) {                                       // accumulator fully read: release it
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&accempty[a]);
-            }
-            float mine[16], other[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float send = __uint_as_float(odd ? v[i] : v[16 + (i ^ 8)]);
-              mine[i] = __uint_as_float(odd ? v[16 + (i ^ 8)] : v[i]);
-              other[i] = __shfl_xor_sync(0xffffffffu, send, 1);
-            }
-            unsigned char* buf = epi + h * 4096;
-            const int tau_c = tau_h + c * 32;
-            // (re, im) = (mine, other) on even lanes, (other, mine) on odd lanes
+          for (int kb = 0; kb < 2; ++kb) {
+            const int r = kb ? tr1 : tr0;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float r0 = odd ? other[2 * q] : mine[2 * q], i0 = odd ? mine[2 * q] : other[2 * q];
-              const float r1 = odd ? other[2 * q + 1] : mine[2 * q + 1], i1 = odd ? mine[2 * q + 1] : other[2 * q + 1];
-              *reinterpret_cast<float4*>(buf + woff + ((q ^ sw) << 4)) = make_float4(r0, i0, r1, i1);
-            }
-            if (p.want_peaks && valid) {
-              float m2[16];
-              float mx = -1.f;
-#pragma unroll
-              for (int i = 0; i < 16; ++i) { m2[i] = mag2f(mine[i], other[i]); mx = fmaxf(mx, m2[i]); }
-              if (mx > bm2) {
-                // smallest lag attaining mx: slot i <-> lag (odd ? 16 + (i ^ 8) : i)
-                int bl = 0x7fffffff;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  const int lag = odd ? 16 + (i ^ 8) : i;
-                  bl = (m2[i] == mx) ? min(bl, lag) : bl;
-                }
-                // value from this thread's own staging write: row r, lag bl
-                const float2 z = *reinterpret_cast<const float2*>(
-                    buf + (bl >> 4) * 2048 + r * 128 + (((((bl & 15) >> 1) ^ (r & 7))) << 4) + (bl & 1) * 8);
-                bm2 = mx; btau = tau_c + bl; bre = z.x; bim = z.y;
-              }
+            for (int rep = 0; rep < 4; ++rep) {
+              const uint32_t* q = v + 16 * kb + 4 * rep;
+              const int ch = ta + 4 * (rep & 1);
+              *reinterpret_cast<float4*>(buf + (rep >> 1) * 2048 + r * 128 + ((ch ^ (r & 7)) << 4)) =
+                  make_float4(__uint_as_float(q[0]), __uint_as_float(q[2]), __uint_as_float(q[1]), __uint_as_float(q[3]));
             }
           }
-          const long long _e2 = TC_CLOCK();
           fence_proxy_async_smem();
           __syncwarp();
-          // warp-uniform operands (broadcast, so the TMA operands live in uniform registers)
-          const int u_tau = __shfl_sync(0xffffffffu, tau_h + c2 * 64, 0);
+          const int u_tau = __shfl_sync(0xffffffffu, tau_c, 0);
           const int u_ti = __shfl_sync(0xffffffffu, ti, 0);
           const int u_t0 = __shfl_sync(0xffffffffu, t0, 0);
           const int u_row = __shfl_sync(0xffffffffu, un.row, 0);
-          const uint32_t u_sa = __shfl_sync(0xffffffffu, smem_u32(epi), 0);
+          const uint32_t u_sa = __shfl_sync(0xffffffffu, smem_u32(buf), 0);
           if (lane == 0) {
             if (p.want_corr) {
               tma_store_4d(&p.tmap, u_sa, u_tau, u_ti, u_t0, u_row);
               tma_store_4d(&p.tmap, u_sa + 2048, u_tau + 16, u_ti, u_t0, u_row);
-              tma_store_4d(&p.tmap, u_sa + 4096, u_tau + 32, u_ti, u_t0, u_row);
-              tma_store_4d(&p.tmap, u_sa + 6144, u_tau + 48, u_ti, u_t0, u_row);
             }
-            bulk_commit();
+            bulk_commit();                                      // (possibly empty) group per chunk
           }
-          e_st += TC_CLOCK() - _e2;
+          if (p.want_peaks) {
+#pragma unroll
+            for (int kb = 0; kb < 2; ++kb) {
+              float m2[8];
+              float mx = -1.f;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {                     // i = 2 rep + j: lag 8 rep + 2 ta + j
+                const uint32_t* q = v + 16 * kb + 4 * (i >> 1);
+                m2[i] = mag2f(__uint_as_float(q[i & 1]), __uint_as_float(q[2 + (i & 1)]));
+                mx = fmaxf(mx, m2[i]);
+              }
+              if (mx > bm2[kb]) {
+                int bi = 7;
+#pragma unroll
+                for (int i = 6; i >= 0; --i) bi = (m2[i] == mx) ? i : bi;
+                float vr = 0.f, vi = 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const uint32_t* q = v + 16 * kb + 4 * (i >> 1);
+                  vr = (i == bi) ? __uint_as_float(q[i & 1]) : vr;
+                  vi = (i == bi) ? __uint_as_float(q[2 + (i & 1)]) : vi;
+                }
+                bm2[kb] = mx; btau[kb] = tau_c + 8 * (bi >> 1) + 2 * ta + (bi & 1); bre[kb] = vr; bim[kb] = vi;
+              }
+            }
+          }
         }
         if (p.want_peaks) {
-          const float om2 = __shfl_xor_sync(0xffffffffu, bm2, 1);
-          const int otau = __shfl_xor_sync(0xffffffffu, btau, 1);
-          const float ore = __shfl_xor_sync(0xffffffffu, bre, 1);
-          const float oim = __shfl_xor_sync(0xffffffffu, bim, 1);
-          if (beats(om2, otau, bm2, btau)) { bm2 = om2; btau = otau; bre = ore; bim = oim; }
-          if (!odd && valid) {
-            PeakF b;
-            b.m2 = bm2; b.tau = btau; b.re = bre; b.im = bim;
-            partials[(((size_t)un.row * p.n_t + t0 + r) * (p.J + 1) + ti) * (2 * p.ntiles) + 2 * un.tile + hh] = b;
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {            // the 4 threads (ta) of a template
+              const float om2 = __shfl_xor_sync(0xffffffffu, bm2[kb], off);
+              const int otau = __shfl_xor_sync(0xffffffffu, btau[kb], off);
+              const float ore = __shfl_xor_sync(0xffffffffu, bre[kb], off);
+              const float oim = __shfl_xor_sync(0xffffffffu, bim[kb], off);
+              if (beats(om2, otau, bm2[kb], btau[kb])) { bm2[kb] = om2; btau[kb] = otau; bre[kb] = ore; bim[kb] = oim; }
+            }
+            const int t = t0 + (kb ? tr1 : tr0);
+            if (ta == 0 && t < p.n_t) {
+              PeakF b;
+              b.m2 = bm2[kb]; b.tau = btau[kb]; b.re = bre[kb]; b.im = bim[kb];
+              partials[(((size_t)un.row * p.n_t + t) * (p.J + 1) + ti) * (2 * p.ntiles) + 2 * un.tile + hh] = b;
+            }
           }
         }
       }
@@ -682,8 +687,7 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
     if (lane == 0) bulk_wait_all();
     __syncwarp();
     if (p.prof && blockIdx.x == 0 && lane == 0)
-      printf("[tc prof] epilogue warp %d: total %lld  wait_accfull %lld  ldtm %lld  bulkwait %lld  sts+tma %lld\n", warp,
-             TC_CLOCK() - t_start, w_acc, e_ld, e_bw, e_st);
+      printf("[tc prof] epilogue warp %d: total %lld  wait_accfull %lld\n", warp, TC_CLOCK() - t_start, w_acc);
   }
   tc_fence_before();
   __syncthreads();
