@@ -267,6 +267,30 @@ def main():
     k1_ms = float(np.median(k1_ms))
     k2_ms = float(np.median(k2_ms))
 
+    # variants (not the headline): fused analyze->correlate->peaks without the band round
+    # trip and the peaks-only mode, CUDA events on the same stream
+    variants = {}
+    def time_fn(fn, n):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+    nv = max(3, min(args.steps, 20))
+    variants["peaks_only_ms"] = time_fn(lambda: (plan.analyze(d_rows, R, bands, stream),
+                                                 plan.correlate_peaks(bands, R, None, lag, val, want_corr=False,
+                                                                      stream=stream)), nv)
+    if plan.fused_available():
+        variants["fused_ms"] = time_fn(lambda: plan.analyze_correlate(d_rows, R, corr, lag, val, stream=stream), nv)
+        variants["fused_peaks_only_ms"] = time_fn(
+            lambda: plan.analyze_correlate(d_rows, R, None, lag, val, want_corr=False, stream=stream), nv)
+    for k in list(variants):
+        variants[k.replace("_ms", "_samples_per_s")] = world * R * cfg.N / (variants[k] * 1e-3)
+
     # timed region: K steps, barrier + sync on both sides, max over ranks
     if world > 1:
         dist.barrier()
@@ -370,6 +394,7 @@ def main():
         "roofline": roof,
         "stages": stages,
         "tensor_cores": tc,
+        "variants": variants,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }

@@ -141,6 +141,19 @@ sidwt_status sidwt_peaks(sidwt_plan plan, const void* d_corr, int64_t rows, int3
 sidwt_status sidwt_correlate_peaks(sidwt_plan plan, const void* d_bands, int64_t rows,
                                    void* d_corr, int32_t* d_lag, void* d_val, void* stream);
 
+/* Fused analyze -> correlate -> peaks (single-template plans): the same outputs as
+ * sidwt_analyze followed by sidwt_correlate_peaks (corr and lag/val bit-identical), but
+ * the bands never leave the chip: each CTA lifts its tile of the row (plus the
+ * correlation reach) in shared memory and correlates level by level.
+ * d_rows as for sidwt_analyze; d_corr may be NULL (peaks only); d_lag / d_val as for
+ * sidwt_correlate_peaks.  SIDWT_ERR_RANGE when the plan has no fused tiling (banks of
+ * more than one template, tap tables over 1536 taps, or tiles that do not fit on chip);
+ * sidwt_fused_available tells in advance. */
+sidwt_status sidwt_analyze_correlate(sidwt_plan plan, const void* d_rows, int64_t rows, void* d_corr,
+                                     int32_t* d_lag, void* d_val, void* stream);
+/* 1 if sidwt_analyze_correlate can run for this plan, 0 if not, -1 before template_load. */
+int sidwt_fused_available(sidwt_plan plan);
+
 /* Synthesis by inverse lifting (coarse to fine, eq. (21); the
  * perfect-reconstruction property of the lifting factorisation, PAPER.md:61-63,
  * 173-179): from bands produced by sidwt_analyze, rebuild the approximation band

@@ -136,6 +136,18 @@ class Plan:
         _native.sidwt_correlate_peaks(self.handle, bands, rows, corr, lag, val, self._stream(stream))
         return corr, lag, val
 
+    def fused_available(self) -> bool:
+        return _native.sidwt_fused_available(self.handle) == 1
+
+    def analyze_correlate(self, d_rows, rows: int, corr=None, lag=None, val=None, want_corr=True, stream=None):
+        """Fused analyze -> correlate -> peaks (no band round trip); single-template plans."""
+        if corr is None and want_corr:
+            corr = self.empty_corr(rows)
+        if lag is None:
+            lag, val = self.empty_peaks(rows)
+        _native.sidwt_analyze_correlate(self.handle, d_rows, rows, corr, lag, val, self._stream(stream))
+        return corr, lag, val
+
     def synthesize(self, bands, rows: int, level: int = 0, out=None, stream=None):
         """Inverse lifting: U_level at positions 0..N-1 ([rows][N][2] float32 / int32)."""
         if out is None:

@@ -13,7 +13,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libsidwt.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sidwt.cu", "kernels.cuh", "lifting.cuh", "corr_tc.cuh")] + [
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sidwt.cu", "kernels.cuh", "lifting.cuh", "corr_tc.cuh", "fused.cuh")] + [
     os.path.join(ROOT, "include", "sidwt.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -28,7 +28,8 @@ STATUS = {0: "SIDWT_OK", 1: "SIDWT_ERR_PARAM", 2: "SIDWT_ERR_LENGTH", 3: "SIDWT_
 
 # every symbol include/sidwt.h declares
 EXPORTS = ["sidwt_plan_create", "sidwt_plan_destroy", "sidwt_template_load", "sidwt_analyze",
-           "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_synthesize", "sidwt_execute_host",
+           "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_analyze_correlate", "sidwt_synthesize",
+           "sidwt_execute_host", "sidwt_fused_available",
            "sidwt_band_stride", "sidwt_band_offset", "sidwt_bands_bytes", "sidwt_corr_bytes",
            "sidwt_template_taps", "sidwt_last_launches", "sidwt_uses_tensor_cores", "sidwt_status_string"]
 
@@ -72,6 +73,9 @@ def lib():
         L.sidwt_correlate_peaks.argtypes = [P, P, I64, P, P, P, P]
         L.sidwt_execute_host.argtypes = [P, P, I64, P, P, P]
         L.sidwt_synthesize.argtypes = [P, P, I64, I, P, P]
+        L.sidwt_analyze_correlate.argtypes = [P, P, I64, P, P, P, P]
+        L.sidwt_fused_available.argtypes = [P]
+        L.sidwt_fused_available.restype = I
         for f in ("sidwt_band_stride", "sidwt_band_offset"):
             getattr(L, f).argtypes = [P]
             getattr(L, f).restype = I64
@@ -147,6 +151,15 @@ def sidwt_peaks(plan, d_corr, rows, d_lag, d_val=None, stream=None):
 def sidwt_correlate_peaks(plan, d_bands, rows, d_corr, d_lag, d_val=None, stream=None):
     _check("sidwt_correlate_peaks", lib().sidwt_correlate_peaks(
         plan, _ptr(d_bands), rows, _ptr(d_corr), _ptr(d_lag), _ptr(d_val), _stream(stream)))
+
+
+def sidwt_analyze_correlate(plan, d_rows, rows, d_corr, d_lag, d_val=None, stream=None):
+    _check("sidwt_analyze_correlate", lib().sidwt_analyze_correlate(
+        plan, _ptr(d_rows), rows, _ptr(d_corr), _ptr(d_lag), _ptr(d_val), _stream(stream)))
+
+
+def sidwt_fused_available(plan) -> int:
+    return lib().sidwt_fused_available(plan)
 
 
 def sidwt_synthesize(plan, d_bands, rows, level, d_out, stream=None):

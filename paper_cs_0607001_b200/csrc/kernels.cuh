@@ -182,7 +182,7 @@ struct AnaParams {
   long long rows;
 };
 
-template <int FAM, int RV, int LH>
+template <int FAM, int RV, int LH, bool BULK = true>
 __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict__ U, typename Dual<FAM>::T* __restrict__ Wst,
                                               int lbuf) {
   typedef typename Dual<FAM>::T T;
@@ -202,7 +202,7 @@ __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict_
     for (int i = 0; i < WIN; ++i) v[i] = src[i * h];
     Dual<FAM>::template run<RV>(v, c, d);
   }
-  if (threadIdx.x == 0 && LH > 0) bulk_wait_read_all();   // staging free again
+  if (BULK && threadIdx.x == 0 && LH > 0) bulk_wait_read_all();   // staging free again
   __syncthreads();
   if (active) {
 #pragma unroll
@@ -211,7 +211,7 @@ __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict_
       Wst[u0 + i * h] = d[i];
     }
   }
-  fence_proxy_async_smem();
+  if (BULK) fence_proxy_async_smem();
   __syncthreads();
 }
 

@@ -15,6 +15,7 @@
 #include "../../include/sidwt.h"
 #include "kernels.cuh"
 #include "corr_tc.cuh"
+#include "fused.cuh"
 
 using namespace sidwt;
 
@@ -59,6 +60,12 @@ struct sidwt_plan_s {
   int last_launches = 0;
   // tensor-core bank path (corr_tc.cuh)
   bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
+  // fused analyze -> correlate -> peaks (single template)
+  bool fused = false;
+  FusParams* fus = nullptr;      // host copy (large: carries the taps)
+  size_t fus_smem = 0;
+  void* d_fpartials = nullptr;
+  size_t fpartials_bytes = 0;
   bool tc = false;
   int tc_sms = 148;
   TcParams tcp{};
@@ -105,6 +112,8 @@ static void free_ws(sidwt_plan_s* p) {
   void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val, &p->d_img};
   for (void** b : bufs) { if (*b) cudaFree(*b); *b = nullptr; }
   for (cudaEvent_t& ev : p->ev) { if (ev) cudaEventDestroy(ev); ev = nullptr; }
+  if (p->d_fpartials) { cudaFree(p->d_fpartials); p->d_fpartials = nullptr; p->fpartials_bytes = 0; }
+  delete p->fus; p->fus = nullptr;
   if (p->s_copy) { cudaStreamDestroy(p->s_copy); p->s_copy = nullptr; }
   if (p->s_comp) { cudaStreamDestroy(p->s_comp); p->s_comp = nullptr; }
   p->partials_bytes = 0;
@@ -281,6 +290,53 @@ static void configure_tc(sidwt_plan_s* p) {
   p->tc = true;
 }
 
+// Fused path: single template, taps in the kernel parameters, and a
+// tile whose on-chip bands + term results fit two CTAs per SM.
+constexpr int kFusNT = 256;
+static void configure_fused(sidwt_plan_s* p) {
+  p->fused = false;
+  if (p->n_t != 1 || !p->ctaps) return;
+  if (!p->fus) p->fus = new (std::nothrow) FusParams();
+  if (!p->fus) return;
+  FusParams& f = *p->fus;
+  const int J = p->J;
+  int fML = 0, fMR = 0;
+  for (int i = 0; i <= J; ++i) {
+    const int g = 1 << (i < J ? i + 1 : J);
+    fML = std::max(fML, -g * p->kmin[i]);
+    fMR = std::max(fMR, g * (p->kmin[i] + p->cnt[i] - 1));
+  }
+  const Reach rc = dual_reach(p->fam);
+  const int maxL = std::max(rc.lowL, rc.hiL);
+  const int64_t halo_l = rup((int64_t)maxL * ((1LL << J) - 1), 4);
+  const int64_t halo_r = std::max<int64_t>((int64_t)rc.lowR * ((1LL << J) - 1),
+                                           (int64_t)rc.lowR * ((1LL << (J - 1)) - 1) + (int64_t)rc.hiR * (1LL << (J - 1)));
+  int HL = 1, HR = 3;
+  if (p->fam == F97) { HL = Dual<F97>::HL; HR = Dual<F97>::HR; }
+  else if (p->fam == FD4) { HL = Dual<FD4>::HL; HR = Dual<FD4>::HR; }
+  const int64_t htop = 1LL << (J - 1);
+  const int64_t padl = rup(HL * htop, 4), padr = rup((kRV - 1 + HR) * htop, 4);
+  for (int64_t TT = std::min<int64_t>(p->N, 2048); TT >= 256 && TT >= (1LL << J); TT >>= 1) {
+    const int64_t lbuf = rup(halo_l + fML + TT + fMR + halo_r, 4);
+    int64_t threads = 0;
+    for (int sl = 1; sl <= J; ++sl) {
+      const int64_t h = 1LL << (sl - 1);
+      threads = std::max(threads, h * cdiv(cdiv(lbuf, h), kRV));
+    }
+    const int64_t per = padl + 2 * (lbuf + padr);
+    const size_t smem = (size_t)rup(2 * per * 4, 16) + (size_t)(J + 1) * TT * 8;
+    if (threads > kFusNT || smem > 110 * 1024) continue;
+    f.N = (int)p->N; f.J = J; f.ext = p->ext; f.TT = (int)TT; f.ntiles = (int)(p->N / TT);
+    f.fML = fML; f.halo_l = (int)halo_l; f.lbuf = (int)lbuf; f.padl = (int)padl; f.padr = (int)padr;
+    f.taps_per_t = p->taps_per_t;
+    for (int i = 0; i <= J; ++i) f.term[i] = p->cor.term[i];
+    memcpy(f.ctap, p->cor.ctap, sizeof(f.ctap));
+    p->fus_smem = smem;
+    p->fused = true;
+    return;
+  }
+}
+
 static sidwt_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return SIDWT_OK;
   if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); return SIDWT_ERR_OOM; }
@@ -332,6 +388,7 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
     if (e != cudaSuccess) { cudaFree(p->d_taps); p->d_taps = nullptr; return cuda_status(e); }
     p->ctaps = true;
   }
+  configure_fused(p);
   configure_tc(p);
   if (p->tc) {
     const size_t img_bytes = (size_t)p->tcp.n_mt * p->tcp.total_ksteps * 8192;
@@ -518,6 +575,57 @@ sidwt_status sidwt_correlate_peaks(sidwt_plan p, const void* d_bands, int64_t ro
   if (st != SIDWT_OK) return st;
   return correlate_impl(p, d_bands, rows, d_corr, d_lag, d_val, true, static_cast<cudaStream_t>(stream));
 }
+
+template <int FAM>
+static cudaError_t launch_fused(sidwt_plan_s* p, const void* rows_in, int64_t rows, void* corr, bool peaks, cudaStream_t s) {
+  auto kern = k_fused<FAM, kRV, kQ, kFusNT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->fus_smem);
+  if (e != cudaSuccess) return e;
+  FusParams& f = *p->fus;
+  f.rows = rows;
+  f.want_corr = corr != nullptr;
+  f.want_peaks = peaks;
+  kern<<<(unsigned)(rows * f.ntiles), kFusNT, p->fus_smem, s>>>(rows_in, corr, p->d_fpartials, f);
+  return cudaGetLastError();
+}
+
+sidwt_status sidwt_analyze_correlate(sidwt_plan p, const void* d_rows, int64_t rows, void* d_corr, int32_t* d_lag,
+                                     void* d_val, void* stream) {
+  if (!p || !d_rows || !d_lag) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  if (!p->fused) return SIDWT_ERR_RANGE;
+  if (rows * p->fus->ntiles > 0x7fffffffLL) return SIDWT_ERR_RANGE;
+  const size_t rec = is_int(p) ? sizeof(PeakI) : sizeof(PeakF);
+  const size_t need = (size_t)p->batch * (p->J + 1) * p->fus->ntiles * rec;
+  if (p->fpartials_bytes < need) {
+    if (p->d_fpartials) cudaFree(p->d_fpartials);
+    p->d_fpartials = nullptr;
+    p->fpartials_bytes = 0;
+    cudaError_t e = cudaMalloc(&p->d_fpartials, need);
+    if (e != cudaSuccess) return cuda_status(e);
+    p->fpartials_bytes = need;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (p->fam) {
+    case F53: e = launch_fused<F53>(p, d_rows, rows, d_corr, true, s); break;
+    case F97: e = launch_fused<F97>(p, d_rows, rows, d_corr, true, s); break;
+    case FD4: e = launch_fused<FD4>(p, d_rows, rows, d_corr, true, s); break;
+    default:  e = launch_fused<FI53>(p, d_rows, rows, d_corr, true, s); break;
+  }
+  if (e == cudaSuccess) {
+    const int64_t count = rows * (p->J + 1);
+    const unsigned blocks = (unsigned)cdiv(count, 8);
+    if (is_int(p)) k_peaks_finalize<true><<<blocks, 256, 0, s>>>(p->d_fpartials, p->fus->ntiles, count, d_lag, d_val);
+    else k_peaks_finalize<false><<<blocks, 256, 0, s>>>(p->d_fpartials, p->fus->ntiles, count, d_lag, d_val);
+    e = cudaGetLastError();
+  }
+  p->last_launches = 2;
+  return cuda_status(e);
+}
+
+int sidwt_fused_available(sidwt_plan p) { return (p && p->loaded) ? (p->fused ? 1 : 0) : -1; }
 
 sidwt_status sidwt_peaks(sidwt_plan p, const void* d_corr, int64_t rows, int32_t* d_lag, void* d_val, void* stream) {
   if (!p || !d_corr || !d_lag) return SIDWT_ERR_PARAM;

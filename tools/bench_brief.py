@@ -11,3 +11,6 @@ print(sys.argv[1].split("/")[-1], "| %.3g samples/s" % d["value"], "| ms/step %.
       "| corr %.3f ms %.1f TF" % (c.get("ms", 0), (c.get("alu") or c.get("tensor") or {}).get("achieved", 0)),
       "| e2e %s" % (d.get("e2e", {}) or {}).get("value"), "| cpu %s" % (d.get("cpu_baseline", {}) or {}).get("value"),
       "| clocks", d.get("clocks"))
+v = d.get("variants") or {}
+if v:
+    print("   variants:", {k: round(x, 3) for k, x in v.items() if k.endswith("_ms")})
