@@ -80,6 +80,18 @@ typedef enum {
     SIDWT_EXT_SYMMETRIC = 1   /* whole-sample symmetric about 0 and N-1 (period 2N-2)   */
 } sidwt_ext;
 
+/* Which signal carries the redundant (shift-invariant) tree (DESIGN.md R-D7):
+ *  RECEIVED_TREE (default, the north star): the received row is decomposed at every shift,
+ *    the template critically sampled: corr_s[tau] = < A_s x, C_s (ybar shifted by tau) >.
+ *  TEMPLATE_TREE (the paper's literal orientation, eq. (20)): the
+ *    template is decomposed at every shift, the received row critically sampled:
+ *    corr_s[tau] = < A_s (x delayed by tau), C_s ybar >.  Equal to the default at s = 0 and
+ *    at tau = 0 mod 2^s, different in between.  Float families; SIMT correlation. */
+typedef enum {
+    SIDWT_ORIENT_RECEIVED_TREE = 0,
+    SIDWT_ORIENT_TEMPLATE_TREE = 1
+} sidwt_orientation;
+
 #define SIDWT_MAX_LEVELS 16
 
 /* Create a plan.  filter: sidwt_filter; levels J >= 1 with 2^J <= N; N a power
@@ -88,6 +100,10 @@ typedef enum {
  * works on a machine without a GPU.  *out receives the plan. */
 sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t N,
                                int64_t batch, int ext);
+
+/* Select the orientation (sidwt_orientation) before sidwt_template_load.  PARAM for an
+ * unknown value or TEMPLATE_TREE with the integer family; STATE after template_load. */
+sidwt_status sidwt_plan_set_orientation(sidwt_plan plan, int orientation);
 
 /* Free the plan and every device buffer it owns.  NULL is accepted. */
 sidwt_status sidwt_plan_destroy(sidwt_plan plan);

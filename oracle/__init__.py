@@ -50,6 +50,7 @@ def lib():
         L.oracle_run.argtypes = [i, i, i, i, i, P, i, i, P, i, i, P, P, P, P, i]
         L.oracle_max_threads.restype = i
         L.oracle_approx.argtypes = [i, i, i, i, P, i, i, i, P, i]
+        L.oracle_run_paper.argtypes = [i, i, i, i, i, P, i, i, P, P, P, P, i]
         _lib = L
     return _lib
 
@@ -183,6 +184,24 @@ def approx(family: int, ext: int, N: int, y: np.ndarray, s: int, p_lo: int = 0, 
     if lib().oracle_approx(family, ext, N, y.shape[0], _p(y), s, p_lo, p_hi, _p(out), nthreads) != 0:
         raise ValueError("oracle_approx rejected its arguments")
     return out
+
+
+def run_paper(family: int, J: int, ext: int, N: int, y: np.ndarray, x: np.ndarray, nthreads: int = 0):
+    """The paper's orientation: corr[rows][n_t][J+1][N] of
+    <A_s (x delayed by tau), C_s ybar>, lag and val; float families only."""
+    y = np.ascontiguousarray(y, dtype=np.complex128)
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    if y.ndim == 1:
+        y = y[None]
+    if x.ndim == 1:
+        x = x[None]
+    rows, n_t, T = y.shape[0], x.shape[0], x.shape[1]
+    cr = np.zeros((rows, n_t, J + 1, N), np.complex128)
+    lag = np.zeros((rows, n_t, J + 1), np.int32)
+    val = np.zeros((rows, n_t, J + 1), np.complex128)
+    if lib().oracle_run_paper(family, J, ext, N, rows, _p(y), T, n_t, _p(x), _p(cr), _p(lag), _p(val), nthreads) != 0:
+        raise ValueError("oracle_run_paper rejected its arguments")
+    return dict(corr=cr, lag=lag, val=val)
 
 
 def max_threads() -> int:

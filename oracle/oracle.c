@@ -594,6 +594,93 @@ int oracle_approx(int family, int ext, int N, int rows, const void* y, int s, in
     return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* The paper's orientation (eq. (20)):  */
+/* the template carries the redundant tree, the received row is critically        */
+/* sampled: corr^P_s[tau] = < A_s S_{-tau} x , C_s ybar >, with S_{-tau} x[n] =     */
+/* x[n - tau] (the template delayed by tau), A_s its analysis approximation and    */
+/* C_s ybar = branch 0 of the received tree (dual analysis).  Plain definition:     */
+/* one Mallat pyramid of the delayed template per lag.  Float families only.        */
+/* ------------------------------------------------------------------------ */
+static void run_row_paper(int family, int J, int ext, int N, const cplx* y, int T, int n_t, const cplx* x,
+                          cplx* corr, int32_t* lag, cplx* val) {
+    filt_t lp;
+    get_filter(family, OR_DUAL, OR_LOWPASS, &lp);
+    int P[21];
+    cplx* c[21];
+    P[0] = (ext == OR_PERIODIC) ? N : (N == 1 ? 1 : 2 * N - 2);
+    c[0] = (cplx*)malloc(sizeof(cplx) * P[0]);
+    for (int n = 0; n < P[0]; n++) c[0][n] = y[ext_index(ext, N, n)];
+    for (int s = 1; s <= J; s++) {                  /* branch 0: even child of branch 0 */
+        P[s] = out_period(P[s - 1]);
+        c[s] = (cplx*)malloc(sizeof(cplx) * P[s]);
+        mallat_periodic(&lp, c[s - 1], P[s - 1], c[s]);
+    }
+    cplx* cs = (cplx*)calloc((size_t)n_t * (J + 1) * N, sizeof(cplx));
+    cplx* xs = (cplx*)malloc(sizeof(cplx) * T);
+    filt_t alp;
+    get_filter(family, OR_ANALYSIS, OR_LOWPASS, &alp);
+    for (int t = 0; t < n_t; t++) {
+        memcpy(xs, x + (long)t * T, sizeof(cplx) * T);
+        for (long tau = 0; tau < N; tau++) {
+            /* analysis approximations a_s of the delayed template x[n - tau], support
+               [tau, tau + T - 1] at level 0 (O3 on the shifted origin) */
+            cplx* a[21];
+            int alo[21], ahi[21];
+            a[0] = xs; alo[0] = (int)tau; ahi[0] = (int)tau + T - 1;
+            for (int s = 1; s <= J; s++) {
+                int lo = alo[s - 1], hi = ahi[s - 1];
+                int klo = (int)ceildiv(lo + alp.lo, 2), khi = (int)floordiv(hi + alp.hi, 2);
+                a[s] = (cplx*)calloc((size_t)(khi - klo + 1), sizeof(cplx));
+                for (int k = klo; k <= khi; k++) {
+                    cplx acc = 0;
+                    for (int m = alp.lo; m <= alp.hi; m++) {
+                        long n = 2L * k - m;
+                        if (n >= lo && n <= hi) acc += fget(&alp, m) * a[s - 1][n - lo];
+                    }
+                    a[s][k - klo] = acc;
+                }
+                alo[s] = klo; ahi[s] = khi;
+            }
+            for (int s = 0; s <= J; s++) {
+                cplx acc = 0;
+                for (int k = alo[s]; k <= ahi[s]; k++) acc += conj(a[s][k - alo[s]]) * c[s][imod(k, P[s])];
+                cs[((long)t * (J + 1) + s) * N + tau] = acc;
+            }
+            for (int s = 1; s <= J; s++) free(a[s]);
+        }
+    }
+    free(xs);
+    for (int s = 0; s <= J; s++) free(c[s]);
+    for (int t = 0; t < n_t; t++)
+        for (int s = 0; s <= J; s++) {
+            const cplx* cc = cs + ((long)t * (J + 1) + s) * N;
+            if (corr) memcpy(corr + ((long)t * (J + 1) + s) * N, cc, sizeof(cplx) * N);
+            long best = 0; double bv = -1.0;
+            for (long tau = 0; tau < N; tau++) {
+                double m = creal(cc[tau]) * creal(cc[tau]) + cimag(cc[tau]) * cimag(cc[tau]);
+                if (m > bv) { bv = m; best = tau; }
+            }
+            if (lag) lag[t * (J + 1) + s] = (int32_t)best;
+            if (val) val[t * (J + 1) + s] = cc[best];
+        }
+    free(cs);
+}
+
+int oracle_run_paper(int family, int J, int ext, int N, int rows, const void* y, int T, int n_t, const void* x,
+                     void* corr, int32_t* lag, void* val, int nthreads) {
+    if (family < 0 || family > 2 || J < 1 || J > 20 || N < 2 || (N & (N - 1)) || (1L << J) > N) return -1;
+    if (T < 1 || T > N || n_t < 1 || rows < 0) return -1;
+    if (ext != OR_PERIODIC && ext != OR_SYMMETRIC) return -1;
+    if (nthreads <= 0) nthreads = oracle_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+    for (int r = 0; r < rows; r++)
+        run_row_paper(family, J, ext, N, (const cplx*)y + (long)r * N, T, n_t, (const cplx*)x,
+                      corr ? (cplx*)corr + (long)r * n_t * (J + 1) * N : NULL, lag ? lag + (long)r * n_t * (J + 1) : NULL,
+                      val ? (cplx*)val + (long)r * n_t * (J + 1) : NULL);
+    return 0;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

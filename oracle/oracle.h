@@ -71,6 +71,13 @@ int oracle_run(int family, int J, int ext, int N, int rows, const void* y,
 int oracle_approx(int family, int ext, int N, int rows, const void* y, int s, int p_lo, int p_hi, void* out,
                   int nthreads);
 
+/* The paper's orientation (template carries the redundant tree, received row critically
+ * sampled; eq. (20)): corr[rows][n_t][J+1][N] of
+ * < A_s (x delayed by tau), C_s ybar > and its peaks, by the plain definition (one Mallat
+ * pyramid of the delayed template per lag).  Float families only; -1 otherwise. */
+int oracle_run_paper(int family, int J, int ext, int N, int rows, const void* y, int T, int n_t, const void* x,
+                     void* corr, int32_t* lag, void* val, int nthreads);
+
 int oracle_max_threads(void);
 
 #ifdef __cplusplus

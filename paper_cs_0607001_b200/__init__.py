@@ -11,21 +11,26 @@ import numpy as np
 
 from . import _native
 from ._native import (SIDWT_CDF97, SIDWT_DAUB4_CAUSAL, SIDWT_EXT_PERIODIC, SIDWT_EXT_SYMMETRIC,  # noqa: F401
-                      SIDWT_LEGALL53, SIDWT_LEGALL53_INT, SidwtError)
+                      SIDWT_LEGALL53, SIDWT_LEGALL53_INT, SIDWT_ORIENT_RECEIVED_TREE, SIDWT_ORIENT_TEMPLATE_TREE,
+                      SidwtError)
 
 __all__ = ["Plan", "SidwtError", "SIDWT_LEGALL53", "SIDWT_CDF97", "SIDWT_DAUB4_CAUSAL",
-           "SIDWT_LEGALL53_INT", "SIDWT_EXT_PERIODIC", "SIDWT_EXT_SYMMETRIC"]
+           "SIDWT_LEGALL53_INT", "SIDWT_EXT_PERIODIC", "SIDWT_EXT_SYMMETRIC", "SIDWT_ORIENT_RECEIVED_TREE",
+           "SIDWT_ORIENT_TEMPLATE_TREE"]
 
 
 class Plan:
     """Owns one sidwt_plan.  Device tensors are torch tensors on ``device``."""
 
-    def __init__(self, filter: int, levels: int, N: int, batch: int, ext: int, device="cuda"):
+    def __init__(self, filter: int, levels: int, N: int, batch: int, ext: int, device="cuda", orientation: int = 0):
         import torch  # plumbing only
         self.torch = torch
         self.filter, self.levels, self.N, self.batch, self.ext = filter, levels, N, batch, ext
         self.device = torch.device(device)
         self.handle = _native.sidwt_plan_create(filter, levels, N, batch, ext)
+        self.orientation = orientation
+        if orientation:
+            _native.sidwt_plan_set_orientation(self.handle, orientation)
         self.n_templates = 0
         self.T = 0
 

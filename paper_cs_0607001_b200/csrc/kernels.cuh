@@ -51,7 +51,9 @@ __device__ __forceinline__ int ext_index(int n, int N, int ext) {
 struct PyrParams {
   int fam, J, T, n_t, taps_per_t;
   int klo[kMaxTerms], cnt[kMaxTerms], off[kMaxTerms];   // term i: b_{i+1} (i<J), a_J (i=J)
+  int npad[kMaxTerms];                                  // residue stride of a term (paper orientation)
   int scratch_len;                                      // per-thread scratch length (doubles)
+  int nres;                                             // 1, or 2^J residues (paper orientation)
 };
 
 template <typename V>
@@ -102,15 +104,24 @@ __host__ __device__ inline long fl_div2(long a) { return a >= 0 ? a / 2 : -((-a 
 __host__ __device__ inline long cl_div2(long a) { return -fl_div2(-a); }
 
 // table: [n_t][taps_per_t] float2 (or int2); scratch: per thread 4 * scratch_len values
+// nres > 1 (the paper's orientation, template carries the redundant tree): thread residue
+// rho pyramids the template delayed by rho (support [rho, rho + T)); term i keeps the
+// residues rho < 2^{lg_i} at table offset off[i] + rho * npad[i] + (k - klo[i]).
 __global__ void k_template_pyramid(const void* __restrict__ x, void* __restrict__ table,
                                    double* __restrict__ scratch, PyrParams p) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= 2 * p.n_t) return;
-  const int t = gid >> 1, comp = gid & 1;
+  if (gid >= 2 * p.n_t * p.nres) return;
+  const int rho = gid / (2 * p.n_t);
+  const int t = (gid >> 1) % p.n_t, comp = gid & 1;
   const Supp sp = analysis_support(p.fam);
   const bool isint = (p.fam == FI53);
   double* base = scratch + (size_t)gid * 4 * p.scratch_len;
-  long lo = 0, hi = p.T - 1;
+  long lo = rho, hi = rho + p.T - 1;
+  auto slot = [&](int ti) -> int {                          // -1: this residue does not feed term ti
+    if (p.nres == 1) return p.off[ti];
+    const int lg = ti < p.J ? ti + 1 : p.J;
+    return rho < (1 << lg) ? p.off[ti] + rho * p.npad[ti] : -1;
+  };
   if (!isint) {
     double* cur = base;
     double* nxt = base + p.scratch_len;
@@ -125,15 +136,15 @@ __global__ void k_template_pyramid(const void* __restrict__ x, void* __restrict_
       const long klo = (alo < blo ? alo : blo) - 2, khi = (ahi > bhi ? ahi : bhi) + 2;
       analysis_level<double>(p.fam, cur, lo, hi, e, o, klo, khi);
       const int ti = s - 1;
-      for (int i = 0; i < p.cnt[ti]; ++i) {
-        const long k = p.klo[ti] + i;
-        tab[2 * (p.off[ti] + i) + comp] = (float)o[k - klo];
-      }
+      const int sl = slot(ti);
+      if (sl >= 0)
+        for (long k = blo; k <= bhi; ++k) tab[2 * (sl + (k - p.klo[ti])) + comp] = (float)o[k - klo];
       for (long k = alo; k <= ahi; ++k) nxt[k - alo] = e[k - klo];
       double* tmp = cur; cur = nxt; nxt = tmp;
       lo = alo; hi = ahi;
     }
-    for (int i = 0; i < p.cnt[p.J]; ++i) tab[2 * (p.off[p.J] + i) + comp] = (float)cur[p.klo[p.J] + i - lo];
+    const int sl = slot(p.J);
+    for (long k = lo; k <= hi; ++k) tab[2 * (sl + (k - p.klo[p.J])) + comp] = (float)cur[k - lo];
   } else {
     int64_t* cur = reinterpret_cast<int64_t*>(base);
     int64_t* nxt = cur + p.scratch_len;
@@ -515,7 +526,7 @@ __device__ __forceinline__ void corr_last(int rem, const typename std::condition
 // sb[r + g (q + k')] (re plane) and sb[... + plane] (im plane).  No index clamps: the
 // tile holds every value the valid outputs need; outputs past the residue's end (the
 // ragged last q-block) read at most g (Q-1) values past the tile, inside the buffer.
-template <bool INT, int Q>
+template <bool INT, int Q, bool PAPER = false>
 __device__ __forceinline__ void corr_item(const typename std::conditional<INT, int, float>::type* sb, int plane,
                                           const typename std::conditional<INT, int2, float2>::type* tp, int ntap,
                                           int r, int lg, int q0,
@@ -524,7 +535,10 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
   typedef typename std::conditional<INT, unsigned, float>::type A;
   const int g = 1 << lg;
   A wr[Q], wi[Q];
-  const auto* base = sb + r + (q0 << lg);
+  // received-tree orientation: outputs r + g q read W[r + g (q + k)]; the paper's orientation
+  // (template tree) reads the critically sampled received band W[g (q + k)] with the
+  // template's residue-r taps
+  const auto* base = sb + (PAPER ? 0 : r) + (q0 << lg);
 #pragma unroll
   for (int m = 0; m < Q; ++m) {
     wr[m] = (A)base[m << lg];
@@ -541,7 +555,7 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
   corr_last<INT, Q, 1>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ar, ai);
 }
 
-template <bool INT, int Q, int NT, int MINB, bool CT>
+template <bool INT, int Q, int NT, int MINB, bool CT, bool PAPER = false>
 __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
                                                    void* __restrict__ corr, void* __restrict__ partials,
                                                    const __grid_constant__ CorParams p) {
@@ -639,7 +653,7 @@ __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__
       const int r = w & (g - 1);
       const int q0 = (w >> tm.lg) * Q;
       A ar[Q], ai[Q];
-      corr_item<INT, Q>(sb, plane, tbase + tm.toff, tm.ntap, r, tm.lg, q0, ar, ai);
+      corr_item<INT, Q, PAPER>(sb, plane, tbase + tm.toff + (PAPER ? r * tm.npad : 0), tm.ntap, r, tm.lg, q0, ar, ai);
       // eq. (4) suffix sum: corr_ti = corr_{ti+1} + term (outputs r + g (q0 + j))
       const int base = r + (q0 << tm.lg);
       const T2* pp = aprev + base;

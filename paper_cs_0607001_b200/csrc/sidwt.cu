@@ -59,6 +59,7 @@ struct sidwt_plan_s {
   cudaEvent_t ev[10] = {};
   int last_launches = 0;
   // tensor-core bank path (corr_tc.cuh)
+  bool paper = false;            // orientation: template carries the redundant tree
   bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
   // fused analyze -> correlate -> peaks (single template)
   bool fused = false;
@@ -126,6 +127,14 @@ sidwt_status sidwt_plan_destroy(sidwt_plan plan) {
   return SIDWT_OK;
 }
 
+sidwt_status sidwt_plan_set_orientation(sidwt_plan p, int orientation) {
+  if (!p || (orientation != SIDWT_ORIENT_RECEIVED_TREE && orientation != SIDWT_ORIENT_TEMPLATE_TREE)) return SIDWT_ERR_PARAM;
+  if (orientation == SIDWT_ORIENT_TEMPLATE_TREE && is_int(p)) return SIDWT_ERR_PARAM;
+  if (p->loaded) return SIDWT_ERR_STATE;
+  p->paper = orientation == SIDWT_ORIENT_TEMPLATE_TREE;
+  return SIDWT_OK;
+}
+
 int64_t sidwt_band_stride(sidwt_plan p) { return (p && p->loaded) ? p->stride : -1; }
 int64_t sidwt_band_offset(sidwt_plan p) { return (p && p->loaded) ? p->ML : -1; }
 int64_t sidwt_bands_bytes(sidwt_plan p, int64_t rows) {
@@ -145,20 +154,28 @@ int sidwt_uses_tensor_cores(sidwt_plan p) { return (p && p->loaded) ? (p->tc ? 1
 static void configure(sidwt_plan_s* p) {
   const int J = p->J;
   const Supp sp = analysis_support(p->fam);
-  // supports of the critically sampled pyramid (zero-extended template on [0,T))
-  long lo = 0, hi = p->T - 1;
-  for (int s = 1; s <= J; ++s) {
-    const long alo = cl_div2(lo + sp.lLo), ahi = fl_div2(hi + sp.lHi);
-    const long blo = cl_div2(lo + sp.hLo), bhi = fl_div2(hi + sp.hHi);
-    p->kmin[s - 1] = (int)blo; p->cnt[s - 1] = (int)(bhi - blo + 1);
-    lo = alo; hi = ahi;
+  // supports of the critically sampled pyramid (zero-extended template on [0,T)); in the
+  // paper's orientation the union over the template delayed by rho = 0 .. 2^{lg} - 1
+  const int nres = p->paper ? (1 << J) : 1;
+  int kmin[kMaxTerms], kmax[kMaxTerms];
+  for (int i = 0; i <= J; ++i) { kmin[i] = INT32_MAX; kmax[i] = INT32_MIN; }
+  for (int rho = 0; rho < nres; ++rho) {
+    long lo = rho, hi = rho + p->T - 1;
+    for (int s = 1; s <= J; ++s) {
+      const long alo = cl_div2(lo + sp.lLo), ahi = fl_div2(hi + sp.lHi);
+      const long blo = cl_div2(lo + sp.hLo), bhi = fl_div2(hi + sp.hHi);
+      if (rho < (1 << s)) { kmin[s - 1] = std::min<int>(kmin[s - 1], (int)blo); kmax[s - 1] = std::max<int>(kmax[s - 1], (int)bhi); }
+      lo = alo; hi = ahi;
+    }
+    kmin[J] = std::min<int>(kmin[J], (int)lo); kmax[J] = std::max<int>(kmax[J], (int)hi);
   }
-  p->kmin[J] = (int)lo; p->cnt[J] = (int)(hi - lo + 1);
+  for (int i = 0; i <= J; ++i) { p->kmin[i] = kmin[i]; p->cnt[i] = kmax[i] - kmin[i] + 1; }
   int off = 0;
   for (int i = 0; i <= J; ++i) {
     p->npad[i] = (int)rup(p->cnt[i], kQ);
     p->toff[i] = off;
-    off += p->npad[i];
+    const int nr = p->paper ? (1 << (i < J ? i + 1 : J)) : 1;
+    off += nr * p->npad[i];
   }
   p->taps_per_t = off;
   // correlation reach -> band margins (DESIGN.md R-D6 GPU): every band value K2 reads exists.
@@ -243,6 +260,7 @@ static void configure(sidwt_plan_s* p) {
 // template bank (n_t >= 16; SIDWT_TC=0 disables, SIDWT_TC=1 forces it for any n_t).
 static void configure_tc(sidwt_plan_s* p) {
   p->tc = false;
+  if (p->paper) return;
   if (is_int(p) || p->N % kTcTilePair != 0) return;
   const char* env = std::getenv("SIDWT_TC");
   if (env && env[0] == '0') return;
@@ -295,7 +313,7 @@ static void configure_tc(sidwt_plan_s* p) {
 constexpr int kFusNT = 256;
 static void configure_fused(sidwt_plan_s* p) {
   p->fused = false;
-  if (p->n_t != 1 || !p->ctaps) return;
+  if (p->n_t != 1 || !p->ctaps || p->paper) return;
   if (!p->fus) p->fus = new (std::nothrow) FusParams();
   if (!p->fus) return;
   FusParams& f = *p->fus;
@@ -360,18 +378,21 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   const size_t x_bytes = (size_t)n_templates * T * sample_bytes(p);
   PyrParams pp{};
   pp.fam = p->fam; pp.J = p->J; pp.T = (int)T; pp.n_t = n_templates; pp.taps_per_t = p->taps_per_t;
-  for (int i = 0; i <= p->J; ++i) { pp.klo[i] = p->kmin[i]; pp.cnt[i] = p->cnt[i]; pp.off[i] = p->toff[i]; }
+  for (int i = 0; i <= p->J; ++i) {
+    pp.klo[i] = p->kmin[i]; pp.cnt[i] = p->cnt[i]; pp.off[i] = p->toff[i]; pp.npad[i] = p->npad[i];
+  }
   pp.scratch_len = (int)T + 64;
+  pp.nres = p->paper ? (1 << p->J) : 1;
   void* d_x = nullptr;
   double* d_scr = nullptr;
   cudaError_t e = cudaMalloc(&p->d_taps, tab_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&d_x, x_bytes);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&d_scr, (size_t)2 * n_templates * 4 * pp.scratch_len * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&d_scr, (size_t)2 * n_templates * pp.nres * 4 * pp.scratch_len * sizeof(double));
   if (e == cudaSuccess) e = cudaMemset(p->d_taps, 0, tab_bytes);
   if (e == cudaSuccess) e = cudaMemcpy(d_x, host_templates, x_bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
     const int threads = 64;
-    k_template_pyramid<<<(unsigned)cdiv(2 * n_templates, threads), threads>>>(d_x, p->d_taps, d_scr, pp);
+    k_template_pyramid<<<(unsigned)cdiv(2 * n_templates * pp.nres, threads), threads>>>(d_x, p->d_taps, d_scr, pp);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -535,7 +556,9 @@ static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t
   void (*kern)(const void*, const void*, void*, void*, const CorParams);
   const bool ct = p->ctaps;
   const bool m3 = minb >= 3;
-  if (is_int(p)) {
+  if (p->paper) {                                  // float families only (checked at set_orientation)
+    kern = ct ? k_correlate<false, kQ, kK2NT, 3, true, true> : k_correlate<false, kQ, kK2NT, 3, false, true>;
+  } else if (is_int(p)) {
     if (ct) kern = m3 ? k_correlate<true, kQ, kK2NT, 3, true> : k_correlate<true, kQ, kK2NT, 2, true>;
     else kern = m3 ? k_correlate<true, kQ, kK2NT, 3, false> : k_correlate<true, kQ, kK2NT, 2, false>;
   } else {

@@ -549,3 +549,73 @@ def _ext_index(ext, N, n):
         return n % N
     m = n % (2 * N - 2)
     return m if m < N else 2 * N - 2 - m
+
+
+# ---------------------------------------------------------------- the paper's orientation (NEXT 3)
+
+@pytest.mark.parametrize("fam", FAMS_FLOAT)
+@pytest.mark.parametrize("ext", (O.PERIODIC, O.SYMMETRIC))
+def test_paper_orientation_pins(fam, ext):
+    """corr^P_s[tau] = <A_s S_{-tau} x, C_s ybar>: equal to the textbook
+    correlation at s = 0 (brute force), equal to this build's orientation <A_s x, C_s S_tau ybar>
+    at tau = 0 mod 2^s, and shift-consistent: the lag 2^s m corresponds to shifting
+    the critically sampled coefficients by m (P12)."""
+    N, J, T = 64, 3, 12
+    y = RNG.normal(size=N) + 1j * RNG.normal(size=N)
+    x = RNG.normal(size=T) + 1j * RNG.normal(size=T)
+    rp = O.run_paper(fam, J, ext, N, y[None], x[None])
+    ro = O.run(fam, J, ext, N, y[None], x[None])
+    ref = np.array([sum(np.conj(x[n]) * _extend(y, ext, np.array([n + tau]))[0] for n in range(T))
+                    for tau in range(N)])
+    np.testing.assert_allclose(rp["corr"][0, 0, 0], ref, atol=1e-12)
+    for s in range(J + 1):
+        sel = np.arange(0, N, 2 ** s)
+        np.testing.assert_allclose(rp["corr"][0, 0, s, sel], ro["corr"][0, 0, s, sel], atol=1e-11)
+    # off the 2^s grid the two orientations differ (D7): at least one lag at every s >= 1
+    for s in range(1, J + 1):
+        off = np.setdiff1d(np.arange(N), np.arange(0, N, 2 ** s))
+        assert np.abs(rp["corr"][0, 0, s, off] - ro["corr"][0, 0, s, off]).max() > 1e-6
+
+
+def test_paper_orientation_dense_matrices():
+    """Brute force on a tiny periodic case: A_s and C_s as explicit matrices (level-by-level
+    Mallat operators of the printed filters), corr^P_s[tau] = (A_s S_{-tau} x)^H (C_s y)."""
+    fam, J, N, T = O.LEGALL53, 2, 16, 5
+    y = RNG.normal(size=N) + 1j * RNG.normal(size=N)
+    x = RNG.normal(size=T) + 1j * RNG.normal(size=T)
+    rp = O.run_paper(fam, J, O.PERIODIC, N, y[None], x[None])
+    # analysis operator on a zero-padded line long enough to hold every delayed template
+    L = 64
+    def op(role, Lin):
+        lo, f = O.filt(fam, role, O.LOWPASS)
+        M = np.zeros((Lin // 2, Lin))
+        for k in range(Lin // 2):
+            for i, m in enumerate(range(lo, lo + len(f))):
+                n = 2 * k - m
+                if 0 <= n < Lin:
+                    M[k, n] += f[i]
+        return M
+    # dual operator on the N-periodic received row
+    def op_per(Lin):
+        lo, f = O.filt(fam, O.DUAL, O.LOWPASS)
+        M = np.zeros((Lin // 2, Lin))
+        for k in range(Lin // 2):
+            for i, m in enumerate(range(lo, lo + len(f))):
+                M[k, (2 * k - m) % Lin] += f[i]
+        return M
+    off = 16                                  # origin of the zero-padded template line
+    for s in range(J + 1):
+        A = np.eye(L)
+        C = np.eye(N)
+        for l in range(s):
+            A = op(O.ANALYSIS, L >> l) @ A
+            C = op_per(N >> l) @ C
+        cy = C @ y
+        for tau in range(N):
+            xt = np.zeros(L, complex)
+            xt[off + tau: off + tau + T] = x
+            ax = A @ xt
+            # coefficient k of the padded line <-> k - off / 2^s of the true line (off multiple of 2^s)
+            ks = np.arange(ax.shape[0]) - off // (2 ** s)
+            val = np.sum(np.conj(ax) * cy[np.mod(ks, N >> s)])
+            assert abs(val - rp["corr"][0, 0, s, tau]) < 1e-10, (s, tau)
