@@ -1,0 +1,44 @@
+// Microbenchmark: FP32 FMA throughput on B200 for FFMA (3-register), FFMA with an immediate,
+// and packed FFMA2 (fma.rn.f32x2).  8 independent chains per thread, many warps.
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void k_ffma(float* out, float a, float b, int iters) {
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 0.001f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+  }
+  float s = 0; for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_ffma2(float* out, float a, float b, int iters) {
+  unsigned long long x[8];
+  float2 av = make_float2(a, a), bv = make_float2(b, b);
+  unsigned long long A = *reinterpret_cast<unsigned long long*>(&av), B = *reinterpret_cast<unsigned long long*>(&bv);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { float2 v = make_float2(threadIdx.x * 0.001f + i, i); x[i] = *reinterpret_cast<unsigned long long*>(&v); }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[i]) : "l"(A), "l"(B));
+  }
+  float s = 0; for (int i = 0; i < 8; ++i) { float2 v = *reinterpret_cast<float2*>(&x[i]); s += v.x + v.y; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+int main() {
+  float* d; cudaMalloc(&d, 148 * 8 * 256 * 4);
+  int iters = 20000;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(e0); k_ffma<<<148 * 8, 256>>>(d, 1.0001f, 0.5f, iters); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double fl = 2.0 * 8 * iters * 148.0 * 8 * 256;
+    printf("FFMA  : %.2f ms  %.1f TFLOP/s\n", ms, fl / ms / 1e9);
+    cudaEventRecord(e0); k_ffma2<<<148 * 8, 256>>>(d, 1.0001f, 0.5f, iters); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    fl = 4.0 * 8 * iters * 148.0 * 8 * 256;
+    printf("FFMA2 : %.2f ms  %.1f TFLOP/s\n", ms, fl / ms / 1e9);
+  }
+  return 0;
+}
