@@ -116,7 +116,9 @@ def algorithmic(cfg, plan):
     stride = plan.band_stride
     k1_bytes = N * sb + (J + 1) * 2 * stride * 4
     taps = sum(c for c in plan_counts(plan))
-    k2_flops = cfg.n_templates * N * taps * 8            # complex MAC = 8 real flops
+    # complex MAC = 8 real flops; a real template (zero imaginary taps, e.g. C2's Barker
+    # code) needs 4 (real x complex), and the real-template kernel does exactly those
+    k2_flops = cfg.n_templates * N * taps * (4 if plan.template_is_real() else 8)
     k2_bytes = (J + 1) * 2 * stride * 4 + cfg.n_templates * (J + 1) * N * 8
     return dict(k1_bytes=k1_bytes, k2_flops=k2_flops, k2_bytes=k2_bytes, taps=taps)
 

@@ -209,6 +209,12 @@ int64_t sidwt_template_taps(sidwt_plan plan, void* host_taps, int32_t* kmin, int
  * SIMT pipes, -1 before template_load. */
 int sidwt_uses_tensor_cores(sidwt_plan plan);
 
+/* 1 if every tap of the loaded template bank is real (zero imaginary part, e.g. a Barker
+ * code) and the SIMT correlation runs its real-template variant (2 instead of 4 FMAs per
+ * complex MAC; the skipped products are exact zeros, results unchanged); 0 otherwise; -1
+ * before template_load.  Environment SIDWT_REALT=0 disables the variant. */
+int sidwt_template_is_real(sidwt_plan plan);
+
 /* Number of kernel launches the last analyze / correlate / peaks / correlate_peaks
  * call enqueued (for launch accounting). */
 int sidwt_last_launches(sidwt_plan plan);

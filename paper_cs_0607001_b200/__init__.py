@@ -164,6 +164,9 @@ class Plan:
     def execute_host(self, h_rows, rows: int, h_lag, h_val=None, stream=None):
         _native.sidwt_execute_host(self.handle, h_rows, rows, h_lag, h_val, self._stream(stream))
 
+    def template_is_real(self) -> bool:
+        return _native.sidwt_template_is_real(self.handle) == 1
+
     def uses_tensor_cores(self) -> bool:
         return _native.sidwt_uses_tensor_cores(self.handle) == 1
 

@@ -32,7 +32,8 @@ EXPORTS = ["sidwt_plan_create", "sidwt_plan_set_orientation", "sidwt_plan_destro
            "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_analyze_correlate", "sidwt_synthesize",
            "sidwt_execute_host", "sidwt_fused_available",
            "sidwt_band_stride", "sidwt_band_offset", "sidwt_bands_bytes", "sidwt_corr_bytes",
-           "sidwt_template_taps", "sidwt_last_launches", "sidwt_uses_tensor_cores", "sidwt_status_string"]
+           "sidwt_template_taps", "sidwt_last_launches", "sidwt_uses_tensor_cores", "sidwt_template_is_real",
+           "sidwt_status_string"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -90,6 +91,8 @@ def lib():
         L.sidwt_last_launches.restype = I
         L.sidwt_uses_tensor_cores.argtypes = [P]
         L.sidwt_uses_tensor_cores.restype = I
+        L.sidwt_template_is_real.argtypes = [P]
+        L.sidwt_template_is_real.restype = I
         L.sidwt_status_string.argtypes = [I]
         L.sidwt_status_string.restype = C.c_char_p
         _lib = L
@@ -203,6 +206,10 @@ def sidwt_last_launches(plan) -> int:
 
 def sidwt_uses_tensor_cores(plan) -> int:
     return lib().sidwt_uses_tensor_cores(plan)
+
+
+def sidwt_template_is_real(plan) -> int:
+    return lib().sidwt_template_is_real(plan)
 
 
 def sidwt_status_string(st: int) -> str:

@@ -451,7 +451,9 @@ struct CorParams {
 // j consumes slot (j + kk) % Q; afterwards slot kk is refilled with the value Q taps
 // ahead.  In the last chunk only the refills consumed within the chunk (kk <= REM - 2)
 // are issued.
-template <int Q, int REM, bool LAST>
+// REAL: every template tap has a zero imaginary part (e.g. the Barker code of C2), so the
+// two FMAs with t.y are exact no-ops and are skipped (same results, half the FMAs).
+template <int Q, int REM, bool LAST, bool REAL = false>
 __device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int plane, int g, const float2* __restrict__ tp,
                                              float (&wr)[Q], float (&wi)[Q], float (&ar)[Q], float (&ai)[Q]) {
 #pragma unroll
@@ -462,9 +464,9 @@ __device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int p
     for (int j = 0; j < Q; ++j) {
       const int sl = (j + kk) % Q;
       ar[j] = fmaf(t.x, wr[sl], ar[j]);
-      ar[j] = fmaf(t.y, wi[sl], ar[j]);
+      if (!REAL) ar[j] = fmaf(t.y, wi[sl], ar[j]);
       ai[j] = fmaf(t.x, wi[sl], ai[j]);
-      ai[j] = fmaf(nty, wr[sl], ai[j]);
+      if (!REAL) ai[j] = fmaf(nty, wr[sl], ai[j]);
     }
     if (!LAST || kk < REM - 1) {
       const float* q = pr + kk * g;
@@ -474,7 +476,7 @@ __device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int p
   }
 }
 
-template <int Q, int REM, bool LAST>
+template <int Q, int REM, bool LAST, bool REAL = false>
 __device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int plane, int g, const int2* __restrict__ tp,
                                              unsigned (&wr)[Q], unsigned (&wi)[Q], unsigned (&ar)[Q], unsigned (&ai)[Q]) {
 #pragma unroll
@@ -484,8 +486,13 @@ __device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int pla
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
       const int sl = (j + kk) % Q;
-      ar[j] += tx * wr[sl] + ty * wi[sl];            // wrap-around int32 (exact mod 2^32)
-      ai[j] += tx * wi[sl] + nty * wr[sl];
+      if (REAL) {
+        ar[j] += tx * wr[sl];
+        ai[j] += tx * wi[sl];
+      } else {
+        ar[j] += tx * wr[sl] + ty * wi[sl];          // wrap-around int32 (exact mod 2^32)
+        ai[j] += tx * wi[sl] + nty * wr[sl];
+      }
     }
     if (!LAST || kk < REM - 1) {
       const int* q = pr + kk * g;
@@ -495,19 +502,19 @@ __device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int pla
   }
 }
 
-template <bool INT, int Q, int REM>
+template <bool INT, int Q, int REM, bool REAL = false>
 __device__ __forceinline__ void corr_chunk(const typename std::conditional<INT, int, float>::type* pr, int plane, int g,
                                            const typename std::conditional<INT, int2, float2>::type* tp,
                                            typename std::conditional<INT, unsigned, float>::type (&wr)[Q],
                                            typename std::conditional<INT, unsigned, float>::type (&wi)[Q],
                                            typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
                                            typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
-  if constexpr (INT) corr_chunk_i<Q, REM, true>(pr, plane, g, tp, wr, wi, ar, ai);
-  else corr_chunk_f<Q, REM, true>(pr, plane, g, tp, wr, wi, ar, ai);
+  if constexpr (INT) corr_chunk_i<Q, REM, true, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
+  else corr_chunk_f<Q, REM, true, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
 }
 
 // Last chunk of an item: REM = rem taps (1..Q), dispatched to a compile-time length.
-template <bool INT, int Q, int R>
+template <bool INT, int Q, int R, bool REAL = false>
 __device__ __forceinline__ void corr_last(int rem, const typename std::conditional<INT, int, float>::type* pr, int plane, int g,
                                           const typename std::conditional<INT, int2, float2>::type* tp,
                                           typename std::conditional<INT, unsigned, float>::type (&wr)[Q],
@@ -515,10 +522,10 @@ __device__ __forceinline__ void corr_last(int rem, const typename std::condition
                                           typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
                                           typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
   if constexpr (R >= Q) {
-    corr_chunk<INT, Q, Q>(pr, plane, g, tp, wr, wi, ar, ai);
+    corr_chunk<INT, Q, Q, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
   } else {
-    if (rem == R) corr_chunk<INT, Q, R>(pr, plane, g, tp, wr, wi, ar, ai);
-    else corr_last<INT, Q, R + 1>(rem, pr, plane, g, tp, wr, wi, ar, ai);
+    if (rem == R) corr_chunk<INT, Q, R, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
+    else corr_last<INT, Q, R + 1, REAL>(rem, pr, plane, g, tp, wr, wi, ar, ai);
   }
 }
 
@@ -526,7 +533,7 @@ __device__ __forceinline__ void corr_last(int rem, const typename std::condition
 // sb[r + g (q + k')] (re plane) and sb[... + plane] (im plane).  No index clamps: the
 // tile holds every value the valid outputs need; outputs past the residue's end (the
 // ragged last q-block) read at most g (Q-1) values past the tile, inside the buffer.
-template <bool INT, int Q, bool PAPER = false>
+template <bool INT, int Q, bool PAPER = false, bool REAL = false>
 __device__ __forceinline__ void corr_item(const typename std::conditional<INT, int, float>::type* sb, int plane,
                                           const typename std::conditional<INT, int2, float2>::type* tp, int ntap,
                                           int r, int lg, int q0,
@@ -549,13 +556,13 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
   const auto* pr = base + (Q << lg);
   const int nfull = (ntap - 1) / Q;          // full chunks; the last chunk has 1..Q taps
   for (int c = 0; c < nfull; ++c, pr += Q * g, tp += Q) {
-    if constexpr (INT) corr_chunk_i<Q, Q, false>(pr, plane, g, tp, wr, wi, ar, ai);
-    else corr_chunk_f<Q, Q, false>(pr, plane, g, tp, wr, wi, ar, ai);
+    if constexpr (INT) corr_chunk_i<Q, Q, false, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
+    else corr_chunk_f<Q, Q, false, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
   }
-  corr_last<INT, Q, 1>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ar, ai);
+  corr_last<INT, Q, 1, REAL>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ar, ai);
 }
 
-template <bool INT, int Q, int NT, int MINB, bool CT, bool PAPER = false>
+template <bool INT, int Q, int NT, int MINB, bool CT, bool PAPER = false, bool REAL = false>
 __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
                                                    void* __restrict__ corr, void* __restrict__ partials,
                                                    const __grid_constant__ CorParams p) {
@@ -653,7 +660,7 @@ __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__
       const int r = w & (g - 1);
       const int q0 = (w >> tm.lg) * Q;
       A ar[Q], ai[Q];
-      corr_item<INT, Q, PAPER>(sb, plane, tbase + tm.toff + (PAPER ? r * tm.npad : 0), tm.ntap, r, tm.lg, q0, ar, ai);
+      corr_item<INT, Q, PAPER, REAL>(sb, plane, tbase + tm.toff + (PAPER ? r * tm.npad : 0), tm.ntap, r, tm.lg, q0, ar, ai);
       // eq. (4) suffix sum: corr_ti = corr_{ti+1} + term (outputs r + g (q0 + j))
       const int base = r + (q0 << tm.lg);
       const T2* pp = aprev + base;

@@ -61,6 +61,7 @@ struct sidwt_plan_s {
   // tensor-core bank path (corr_tc.cuh)
   bool paper = false;            // orientation: template carries the redundant tree
   bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
+  bool real_taps = false;        // every template tap has a zero imaginary part
   // fused analyze -> correlate -> peaks (single template)
   bool fused = false;
   FusParams* fus = nullptr;      // host copy (large: carries the taps)
@@ -147,6 +148,7 @@ int64_t sidwt_corr_bytes(sidwt_plan p, int64_t rows) {
 }
 int sidwt_last_launches(sidwt_plan p) { return p ? p->last_launches : 0; }
 int sidwt_uses_tensor_cores(sidwt_plan p) { return (p && p->loaded) ? (p->tc ? 1 : 0) : -1; }
+int sidwt_template_is_real(sidwt_plan p) { return (p && p->loaded) ? (p->real_taps ? 1 : 0) : -1; }
 
 // ---------------------------------------------------------------------------
 // Template load: supports, margins, tiling, and the device pyramid (K0).
@@ -404,10 +406,16 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   }
   // small tap tables travel in the SIMT correlation's kernel parameters (constant cache)
   p->ctaps = false;
+  p->real_taps = false;
   if ((int64_t)n_templates * p->taps_per_t <= kCTaps && !(std::getenv("SIDWT_CTAPS") && std::getenv("SIDWT_CTAPS")[0] == '0')) {
     e = cudaMemcpy(p->cor.ctap, p->d_taps, tab_bytes, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) { cudaFree(p->d_taps); p->d_taps = nullptr; return cuda_status(e); }
     p->ctaps = true;
+    // real template (imaginary bits all +-0 / integer 0): the correlation skips the t.y terms
+    bool real = !(std::getenv("SIDWT_REALT") && std::getenv("SIDWT_REALT")[0] == '0');
+    for (int64_t i = 0; real && i < (int64_t)n_templates * p->taps_per_t; ++i)
+      real = (p->cor.ctap[i].y & 0x7fffffffu) == 0u;
+    p->real_taps = real;
   }
   configure_fused(p);
   configure_tc(p);
@@ -558,6 +566,8 @@ static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t
   const bool m3 = minb >= 3;
   if (p->paper) {                                  // float families only (checked at set_orientation)
     kern = ct ? k_correlate<false, kQ, kK2NT, 3, true, true> : k_correlate<false, kQ, kK2NT, 3, false, true>;
+  } else if (p->real_taps && ct) {                 // real template bank (zero imaginary taps)
+    kern = is_int(p) ? k_correlate<true, kQ, kK2NT, 3, true, false, true> : k_correlate<false, kQ, kK2NT, 3, true, false, true>;
   } else if (is_int(p)) {
     if (ct) kern = m3 ? k_correlate<true, kQ, kK2NT, 3, true> : k_correlate<true, kQ, kK2NT, 2, true>;
     else kern = m3 ? k_correlate<true, kQ, kK2NT, 3, false> : k_correlate<true, kQ, kK2NT, 2, false>;

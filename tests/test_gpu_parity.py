@@ -197,3 +197,23 @@ def test_full_size_c4_sampled():
              lag=lag[ids].cpu().numpy(), val=val[ids].cpu().numpy())
     r = oracle_for(plan, rows[ids], tm)
     compare(plan, g, r)
+
+
+def test_real_template_variant_equals_general_path():
+    """C2's Barker template is real: the real-template correlation (t.y products skipped) gives
+    the same corr and peaks as the general complex kernel (SIDWT_REALT=0)."""
+    import os
+    cfg = W.CONFIGS[2]
+    tm = W.templates(cfg)
+    rows = W.make_rows(cfg, 0, 4, tm)
+    p_real = _plan(cfg, 4, tm)
+    os.environ["SIDWT_REALT"] = "0"
+    try:
+        p_gen = _plan(cfg, 4, tm)
+    finally:
+        os.environ.pop("SIDWT_REALT", None)
+    assert p_real.template_is_real() and not p_gen.template_is_real()
+    g1 = run_gpu(p_real, rows, fused=True)
+    g2 = run_gpu(p_gen, rows, fused=True)
+    assert np.array_equal(g1["corr"], g2["corr"]) and np.array_equal(g1["lag"], g2["lag"])
+    compare(p_real, g1, oracle_for(p_real, rows, tm))
