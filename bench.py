@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--rows", type=int, default=0, help="override batch rows (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the non-headline variant timings")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -272,6 +273,7 @@ def main():
     # variants (not the headline): fused analyze->correlate->peaks without the band round
     # trip and the peaks-only mode, CUDA events on the same stream
     variants = {}
+
     def time_fn(fn, n):
         fn()
         torch.cuda.synchronize()
@@ -283,13 +285,15 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / n
     nv = max(3, min(args.steps, 20))
-    variants["peaks_only_ms"] = time_fn(lambda: (plan.analyze(d_rows, R, bands, stream),
-                                                 plan.correlate_peaks(bands, R, None, lag, val, want_corr=False,
-                                                                      stream=stream)), nv)
-    if plan.fused_available():
-        variants["fused_ms"] = time_fn(lambda: plan.analyze_correlate(d_rows, R, corr, lag, val, stream=stream), nv)
-        variants["fused_peaks_only_ms"] = time_fn(
-            lambda: plan.analyze_correlate(d_rows, R, None, lag, val, want_corr=False, stream=stream), nv)
+    if not args.no_variants:
+        variants["peaks_only_ms"] = time_fn(lambda: (plan.analyze(d_rows, R, bands, stream),
+                                                     plan.correlate_peaks(bands, R, None, lag, val, want_corr=False,
+                                                                          stream=stream)), nv)
+        if plan.fused_available():
+            variants["fused_ms"] = time_fn(lambda: plan.analyze_correlate(d_rows, R, corr, lag, val, stream=stream),
+                                           nv)
+            variants["fused_peaks_only_ms"] = time_fn(
+                lambda: plan.analyze_correlate(d_rows, R, None, lag, val, want_corr=False, stream=stream), nv)
     for k in list(variants):
         variants[k.replace("_ms", "_samples_per_s")] = world * R * cfg.N / (variants[k] * 1e-3)
 

@@ -11,13 +11,13 @@ timeout 600 python bench.py --config 3 --steps 20 > $OUT/bench_${TAG}_c3.json 2>
 timeout 600 python bench.py --config 5 --steps 20 > $OUT/bench_${TAG}_c5.json 2> $OUT/bench_${TAG}_c5.err; echo "bench c5 rc=$?"
 timeout 900 python bench.py --config 4 --steps 3 --no-e2e > $OUT/bench_${TAG}_c4.json 2> $OUT/bench_${TAG}_c4.err; echo "bench c4 rc=$?"
 for c in c2 c3 c5 c4; do python tools/bench_brief.py $OUT/bench_${TAG}_$c.json; done
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-variants"
 timeout 300 $CMD > $OUT/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_analyze|k_correlate" -s 4 -c 2 -o $OUT/prof_$TAG $CMD > $OUT/ncu_full_$TAG.log 2>&1
 echo "ncu rc=$?"
 # tensor-core bank kernel: launch list share and one full capture on a reduced C4 batch
-CMD4="python bench.py --config 4 --rows 256 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+CMD4="python bench.py --config 4 --rows 256 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-variants"
 timeout 300 $CMD4 > $OUT/plain4_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches4_$TAG.csv $CMD4 > $OUT/ncu_launch4_$TAG.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_correlate_tc|k_analyze" -s 2 -c 2 -o $OUT/prof4_$TAG $CMD4 > $OUT/ncu_full4_$TAG.log 2>&1

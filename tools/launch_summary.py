@@ -1,6 +1,6 @@
 """Per-kernel launch count / mean time / share of an ncu --metrics gpu__time_duration.sum csv.
-usage: python tools/launch_summary.py <launches.csv> <title>"""
-import collections, csv, sys
+usage: python tools/launch_summary.py <launches.csv> <title> [exclude-regex]"""
+import collections, csv, re, sys
 rows = list(csv.reader(open(sys.argv[1])))
 i = [k for k, r in enumerate(rows) if 'Kernel Name' in r][0]
 h = rows[i]; data = rows[i + 1:]
@@ -8,6 +8,8 @@ ki, vi, ui = h.index('Kernel Name'), h.index('Metric Value'), h.index('Metric Un
 agg = collections.OrderedDict()
 for r in data:
     if len(r) <= vi:
+        continue
+    if len(sys.argv) > 3 and re.search(sys.argv[3], r[ki]):
         continue
     agg.setdefault(r[ki].split('(')[0], []).append(float(r[vi].replace(',', '')))
 tot = sum(sum(v) for v in agg.values())
