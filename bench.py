@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the non-headline variant timings")
+    ap.add_argument("--two-call", action="store_true", help="time analyze + correlate_peaks as two plain calls")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -246,14 +247,19 @@ def main():
     corr = plan.empty_corr(R)
     lag, val = plan.empty_peaks(R)
 
-    def step():
+    def step_two_call():
         plan.analyze(d_rows, R, bands, stream)
         plan.correlate_peaks(bands, R, corr, lag, val, stream=stream)
 
-    launches_per_step = 1 + 2
+    def step_run():
+        # the library's whole-path call: analysis of row chunk k+1 overlaps correlation of chunk k
+        plan.run(d_rows, R, bands, corr, lag, val, stream=stream)
+
+    step = step_two_call if args.two_call else step_run
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    launches_per_step = plan.last_launches()
 
     # per-kernel timing (CUDA events on the launching stream), separate pass
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -286,6 +292,8 @@ def main():
         return e0.elapsed_time(e1) / n
     nv = max(3, min(args.steps, 20))
     if not args.no_variants:
+        variants["two_call_ms"] = time_fn(step_two_call, nv)
+        variants["run_ms"] = time_fn(step_run, nv)
         variants["peaks_only_ms"] = time_fn(lambda: (plan.analyze(d_rows, R, bands, stream),
                                                      plan.correlate_peaks(bands, R, None, lag, val, want_corr=False,
                                                                           stream=stream)), nv)

@@ -157,6 +157,18 @@ sidwt_status sidwt_peaks(sidwt_plan plan, const void* d_corr, int64_t rows, int3
 sidwt_status sidwt_correlate_peaks(sidwt_plan plan, const void* d_bands, int64_t rows,
                                    void* d_corr, int32_t* d_lag, void* d_val, void* stream);
 
+/* The whole path on device-resident rows: sidwt_analyze then sidwt_correlate_peaks
+ * (a2-a7 of the scope table), with the same outputs, bit for bit.
+ * Environment SIDWT_RUN_CHUNKS=2..16 cuts the rows into chunks, the analysis of chunk
+ * k+1 issued on a high-priority stream owned by the plan while the correlation + peaks
+ * of chunk k run on a low-priority one (default 1 chunk: on B200 the overlap measured
+ * no gain).  The call is stream-ordered on `stream` (the plan's streams are joined by
+ * events before return).  d_bands: caller-owned workspace
+ * as for sidwt_analyze (rows x sidwt_bands_bytes per row), overwritten; d_corr may be
+ * NULL (peaks only); d_lag / d_val as for sidwt_correlate_peaks. */
+sidwt_status sidwt_run(sidwt_plan plan, const void* d_rows, int64_t rows, void* d_bands, void* d_corr,
+                       int32_t* d_lag, void* d_val, void* stream);
+
 /* Fused analyze -> correlate -> peaks (single-template plans): the same outputs as
  * sidwt_analyze followed by sidwt_correlate_peaks (corr and lag/val bit-identical), but
  * the bands never leave the chip: each CTA lifts its tile of the row (plus the

@@ -141,6 +141,18 @@ class Plan:
         _native.sidwt_correlate_peaks(self.handle, bands, rows, corr, lag, val, self._stream(stream))
         return corr, lag, val
 
+    def run(self, d_rows, rows: int, bands=None, corr=None, lag=None, val=None, want_corr=True, stream=None):
+        """Whole path (analyze -> correlate -> peaks) with the analysis of the next row chunk
+        overlapping the correlation of the current one; same outputs as analyze + correlate_peaks."""
+        if bands is None:
+            bands = self.empty_bands(rows)
+        if corr is None and want_corr:
+            corr = self.empty_corr(rows)
+        if lag is None:
+            lag, val = self.empty_peaks(rows)
+        _native.sidwt_run(self.handle, d_rows, rows, bands, corr, lag, val, self._stream(stream))
+        return corr, lag, val
+
     def fused_available(self) -> bool:
         return _native.sidwt_fused_available(self.handle) == 1
 

@@ -29,7 +29,7 @@ STATUS = {0: "SIDWT_OK", 1: "SIDWT_ERR_PARAM", 2: "SIDWT_ERR_LENGTH", 3: "SIDWT_
 
 # every symbol include/sidwt.h declares
 EXPORTS = ["sidwt_plan_create", "sidwt_plan_set_orientation", "sidwt_plan_destroy", "sidwt_template_load", "sidwt_analyze",
-           "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_analyze_correlate", "sidwt_synthesize",
+           "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_run", "sidwt_analyze_correlate", "sidwt_synthesize",
            "sidwt_execute_host", "sidwt_fused_available",
            "sidwt_band_stride", "sidwt_band_offset", "sidwt_bands_bytes", "sidwt_corr_bytes",
            "sidwt_template_taps", "sidwt_last_launches", "sidwt_uses_tensor_cores", "sidwt_template_is_real",
@@ -75,6 +75,7 @@ def lib():
         L.sidwt_peaks.argtypes = [P, P, I64, P, P, P]
         L.sidwt_correlate_peaks.argtypes = [P, P, I64, P, P, P, P]
         L.sidwt_execute_host.argtypes = [P, P, I64, P, P, P]
+        L.sidwt_run.argtypes = [P, P, I64, P, P, P, P, P]
         L.sidwt_synthesize.argtypes = [P, P, I64, I, P, P]
         L.sidwt_analyze_correlate.argtypes = [P, P, I64, P, P, P, P]
         L.sidwt_fused_available.argtypes = [P]
@@ -160,6 +161,11 @@ def sidwt_peaks(plan, d_corr, rows, d_lag, d_val=None, stream=None):
 def sidwt_correlate_peaks(plan, d_bands, rows, d_corr, d_lag, d_val=None, stream=None):
     _check("sidwt_correlate_peaks", lib().sidwt_correlate_peaks(
         plan, _ptr(d_bands), rows, _ptr(d_corr), _ptr(d_lag), _ptr(d_val), _stream(stream)))
+
+
+def sidwt_run(plan, d_rows, rows, d_bands, d_corr, d_lag, d_val=None, stream=None):
+    _check("sidwt_run", lib().sidwt_run(
+        plan, _ptr(d_rows), rows, _ptr(d_bands), _ptr(d_corr), _ptr(d_lag), _ptr(d_val), _stream(stream)))
 
 
 def sidwt_analyze_correlate(plan, d_rows, rows, d_corr, d_lag, d_val=None, stream=None):

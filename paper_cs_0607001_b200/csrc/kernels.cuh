@@ -562,6 +562,54 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
   corr_last<INT, Q, 1, REAL>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ar, ai);
 }
 
+// All items of one term: thread item (r, qb) computes Q outputs of residue r, then the
+// eq. (4) suffix sum corr_ti = corr_{ti+1} + term into the other accumulator buffer.
+// LG >= 0: g = 2^LG is a compile-time constant; LG = -1: runtime lg.
+template <bool INT, int Q, bool PAPER, bool REAL, int LG>
+__device__ __forceinline__ void corr_term(const typename std::conditional<INT, int, float>::type* sb, int plane,
+                                          const typename std::conditional<INT, int2, float2>::type* tp, const Term& tm,
+                                          int lg_rt, int TT, const typename std::conditional<INT, int2, float2>::type* aprev,
+                                          typename std::conditional<INT, int2, float2>::type* anew, bool first) {
+  typedef typename std::conditional<INT, int, float>::type T;
+  typedef typename std::conditional<INT, int2, float2>::type T2;
+  typedef typename std::conditional<INT, unsigned, float>::type A;
+  const int lg = LG >= 0 ? LG : lg_rt;
+  const int g = 1 << lg;
+  const int nq = TT >> lg;
+  const int nqb = (nq + Q - 1) / Q;
+  for (int w = threadIdx.x; w < g * nqb; w += blockDim.x) {
+    const int r = w & (g - 1);
+    const int q0 = (w >> lg) * Q;
+    A ar[Q], ai[Q];
+    corr_item<INT, Q, PAPER, REAL>(sb, plane, tp + (PAPER ? r * tm.npad : 0), tm.ntap, r, lg, q0, ar, ai);
+    // eq. (4) suffix sum: corr_ti = corr_{ti+1} + term (outputs r + g (q0 + j))
+    const int base = r + (q0 << lg);
+    const T2* pp = aprev + base;
+    T2* pn = anew + base;
+    const int nj = min(Q, nq - q0);
+    if (first) {
+#pragma unroll
+      for (int j = 0; j < Q; ++j)
+        if (j < nj) { T2 o; o.x = (T)ar[j]; o.y = (T)ai[j]; pn[j * g] = o; }
+    } else if (nj == Q) {
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const T2 v = pp[j * g];
+        T2 o; o.x = (T)((A)v.x + ar[j]); o.y = (T)((A)v.y + ai[j]);
+        pn[j * g] = o;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < Q; ++j)
+        if (j < nj) {
+          const T2 v = pp[j * g];
+          T2 o; o.x = (T)((A)v.x + ar[j]); o.y = (T)((A)v.y + ai[j]);
+          pn[j * g] = o;
+        }
+    }
+  }
+}
+
 template <bool INT, int Q, int NT, int MINB, bool CT, bool PAPER = false, bool REAL = false>
 __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__ bands, const void* __restrict__ taps,
                                                    void* __restrict__ corr, void* __restrict__ partials,
@@ -651,41 +699,19 @@ __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__
       }
       __syncthreads();
     }
-    // compute term, accumulate into acc[cur^1] = acc[cur] + term
-    const int nq = TT >> tm.lg;
-    const int nqb = (nq + Q - 1) / Q;
+    // compute term, accumulate into acc[cur^1] = acc[cur] + term; the band stride g = 2^lg
+    // is dispatched to a compile-time constant (immediate shared-memory offsets in the tap loop)
     const T2* aprev = acc + (size_t)cur * TT;
     T2* anew = acc + (size_t)(cur ^ 1) * TT;
-    for (int w = threadIdx.x; w < g * nqb; w += blockDim.x) {
-      const int r = w & (g - 1);
-      const int q0 = (w >> tm.lg) * Q;
-      A ar[Q], ai[Q];
-      corr_item<INT, Q, PAPER, REAL>(sb, plane, tbase + tm.toff + (PAPER ? r * tm.npad : 0), tm.ntap, r, tm.lg, q0, ar, ai);
-      // eq. (4) suffix sum: corr_ti = corr_{ti+1} + term (outputs r + g (q0 + j))
-      const int base = r + (q0 << tm.lg);
-      const T2* pp = aprev + base;
-      T2* pn = anew + base;
-      const int nj = min(Q, nq - q0);
-      if (step == 0) {
-#pragma unroll
-        for (int j = 0; j < Q; ++j)
-          if (j < nj) { T2 o; o.x = (T)ar[j]; o.y = (T)ai[j]; pn[j * g] = o; }
-      } else if (nj == Q) {
-#pragma unroll
-        for (int j = 0; j < Q; ++j) {
-          const T2 v = pp[j * g];
-          T2 o; o.x = (T)((A)v.x + ar[j]); o.y = (T)((A)v.y + ai[j]);
-          pn[j * g] = o;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < Q; ++j)
-          if (j < nj) {
-            const T2 v = pp[j * g];
-            T2 o; o.x = (T)((A)v.x + ar[j]); o.y = (T)((A)v.y + ai[j]);
-            pn[j * g] = o;
-          }
-      }
+    const T2* tp = tbase + tm.toff;
+    switch (tm.lg) {
+      case 1: corr_term<INT, Q, PAPER, REAL, 1>(sb, plane, tp, tm, 1, TT, aprev, anew, step == 0); break;
+      case 2: corr_term<INT, Q, PAPER, REAL, 2>(sb, plane, tp, tm, 2, TT, aprev, anew, step == 0); break;
+      case 3: corr_term<INT, Q, PAPER, REAL, 3>(sb, plane, tp, tm, 3, TT, aprev, anew, step == 0); break;
+      case 4: corr_term<INT, Q, PAPER, REAL, 4>(sb, plane, tp, tm, 4, TT, aprev, anew, step == 0); break;
+      case 5: corr_term<INT, Q, PAPER, REAL, 5>(sb, plane, tp, tm, 5, TT, aprev, anew, step == 0); break;
+      case 6: corr_term<INT, Q, PAPER, REAL, 6>(sb, plane, tp, tm, 6, TT, aprev, anew, step == 0); break;
+      default: corr_term<INT, Q, PAPER, REAL, -1>(sb, plane, tp, tm, tm.lg, TT, aprev, anew, step == 0); break;
     }
     __syncthreads();
     if (tma && !dbl && threadIdx.x == 0 && step < p.J) issue(step + 1, 0);

@@ -25,6 +25,7 @@ constexpr int kRV = 15;     // K1 run length (odd: bank-conflict free)
 constexpr int kQ = 9;       // K2 outputs per item (odd: bank-conflict free)
 constexpr int kK2NT = 256;  // K2 threads (Q = 11 with 192 threads measured slower on C2 and C5)
 
+constexpr int kRunChunks = 16;   // sidwt_run: analysis of chunk k+1 overlaps the correlation of chunk k
 constexpr int kPipeChunks = 8;   // execute_host: host->device copy of chunk k overlaps compute of chunk k-1
 
 inline int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -57,11 +58,14 @@ struct sidwt_plan_s {
   // execute_host pipeline
   cudaStream_t s_copy = nullptr, s_comp = nullptr;
   cudaEvent_t ev[10] = {};
+  cudaStream_t s_k1 = nullptr, s_k2 = nullptr;   // sidwt_run: analysis (high priority) / correlation streams
+  cudaEvent_t rev[kRunChunks + 2] = {};
   int last_launches = 0;
   // tensor-core bank path (corr_tc.cuh)
   bool paper = false;            // orientation: template carries the redundant tree
   bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
   bool real_taps = false;        // every template tap has a zero imaginary part
+  int run_chunks = 1;            // sidwt_run default chunk count
   // fused analyze -> correlate -> peaks (single template)
   bool fused = false;
   FusParams* fus = nullptr;      // host copy (large: carries the taps)
@@ -118,6 +122,10 @@ static void free_ws(sidwt_plan_s* p) {
   delete p->fus; p->fus = nullptr;
   if (p->s_copy) { cudaStreamDestroy(p->s_copy); p->s_copy = nullptr; }
   if (p->s_comp) { cudaStreamDestroy(p->s_comp); p->s_comp = nullptr; }
+  if (p->s_k2) { cudaStreamDestroy(p->s_k2); p->s_k2 = nullptr; }
+  if (p->s_k1) { cudaStreamDestroy(p->s_k1); p->s_k1 = nullptr; }
+  for (auto& ev : p->rev)
+    if (ev) { cudaEventDestroy(ev); ev = nullptr; }
   p->partials_bytes = 0;
 }
 
@@ -153,6 +161,7 @@ int sidwt_template_is_real(sidwt_plan p) { return (p && p->loaded) ? (p->real_ta
 // ---------------------------------------------------------------------------
 // Template load: supports, margins, tiling, and the device pyramid (K0).
 // ---------------------------------------------------------------------------
+static void k2_buffers(sidwt_plan_s* p, int Q);
 static void configure(sidwt_plan_s* p) {
   const int J = p->J;
   const Supp sp = analysis_support(p->fam);
@@ -243,17 +252,25 @@ static void configure(sidwt_plan_s* p) {
   CorParams& c = p->cor;
   c.N = (int)p->N; c.J = J; c.ext = p->ext; c.stride = (int)p->stride; c.ML = ML; c.n_t = p->n_t;
   c.TT = (int)TT; c.ntiles = (int)(p->N / TT); c.taps_per_t = p->taps_per_t;
-  int blen_max = 0;
   for (int i = 0; i <= J; ++i) {
     const int lg = i < J ? i + 1 : J;
     c.term[i].band = i; c.term[i].lg = lg; c.term[i].kmin = p->kmin[i];
     c.term[i].npad = p->npad[i]; c.term[i].ntap = p->cnt[i]; c.term[i].toff = p->toff[i];
-    blen_max = std::max<int>(blen_max, (int)TT + (1 << lg) * (p->cnt[i] - 1 + kQ - 1));
   }
+  k2_buffers(p, kQ);
+}
+
+// K2 band tile buffers for items of Q outputs: the tile of a term spans TT + g (ntap - 1)
+// values, plus g (Q - 1) read past it by the ragged last q-block of a residue.
+static void k2_buffers(sidwt_plan_s* p, int Q) {
+  CorParams& c = p->cor;
+  int blen_max = 0;
+  for (int i = 0; i <= c.J; ++i)
+    blen_max = std::max<int>(blen_max, c.TT + (1 << c.term[i].lg) * (c.term[i].ntap - 1 + Q - 1));
   c.balloc = (int)rup(blen_max + 4, 4);          // + alignment shift of the bulk copy
   // double-buffered band tiles when they fit (prefetch overlaps compute), else single
   c.nbuf = 2;
-  auto smem = [&](int nb) { return 16 + rup((int64_t)p->taps_per_t * 8, 128) + (size_t)2 * nb * c.balloc * 4 + (size_t)4 * TT * 4; };
+  auto smem = [&](int nb) { return 16 + rup((int64_t)p->taps_per_t * 8, 128) + (size_t)2 * nb * c.balloc * 4 + (size_t)4 * c.TT * 4; };
   if (smem(2) > 150 * 1024) c.nbuf = 1;
   p->cor_smem = smem(c.nbuf);
 }
@@ -774,6 +791,73 @@ sidwt_status sidwt_execute_host(sidwt_plan p, const void* h_rows, int64_t rows, 
     if (e != cudaSuccess) return cuda_status(e);
   }
   e = cudaEventRecord(ev_done, p->s_comp);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_done, 0);
+  p->last_launches = launches;
+  return cuda_status(e);
+}
+
+// Whole path on device-resident rows (analyze -> correlate -> peaks).  Optionally
+// (SIDWT_RUN_CHUNKS > 1) the rows are cut into chunks: the analysis (HBM-bound) of
+// chunk k+1 runs on a high-priority stream while the correlation (issue-bound) of chunk
+// k runs on a low-priority one.  Measured on B200 (C2, C3, C5): no overlap materialises
+// (the correlation's CTAs hold the SMs' shared memory), so 1 chunk is the default.
+// Same outputs as sidwt_analyze + sidwt_correlate_peaks.
+sidwt_status sidwt_run(sidwt_plan p, const void* d_rows, int64_t rows, void* d_bands, void* d_corr, int32_t* d_lag,
+                       void* d_val, void* stream) {
+  if (!p || !d_rows || !d_bands || !d_lag) return SIDWT_ERR_PARAM;
+  if (!p->loaded) return SIDWT_ERR_STATE;
+  if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int nch = p->run_chunks;
+  if (const char* ev = std::getenv("SIDWT_RUN_CHUNKS")) nch = std::max(1, std::min(kRunChunks, atoi(ev)));
+  nch = (int)std::min<int64_t>(nch, rows);
+  sidwt_status st = ensure_partials(p);
+  if (st != SIDWT_OK) return st;
+  if (nch <= 1) {
+    st = sidwt_analyze(p, d_rows, rows, d_bands, stream);
+    if (st != SIDWT_OK) return st;
+    const int l1 = p->last_launches;
+    st = correlate_impl(p, d_bands, rows, d_corr, d_lag, d_val, true, s);
+    p->last_launches += l1;
+    return st;
+  }
+  cudaError_t e = cudaSuccess;
+  if (!p->s_k1) {
+    int lo = 0, hi = 0;
+    e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&p->s_k1, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&p->s_k2, cudaStreamNonBlocking, lo);
+  }
+  for (int k = 0; e == cudaSuccess && k < kRunChunks + 2; ++k)
+    if (!p->rev[k]) e = cudaEventCreateWithFlags(&p->rev[k], cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_status(e);
+  cudaEvent_t ev_start = p->rev[kRunChunks], ev_done = p->rev[kRunChunks + 1];
+  e = cudaEventRecord(ev_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_k1, ev_start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_k2, ev_start, 0);
+  if (e != cudaSuccess) return cuda_status(e);
+  const int64_t per = cdiv(rows, nch);
+  const size_t sb = sample_bytes(p);
+  const size_t per_row_out = (size_t)p->n_t * (p->J + 1);
+  int launches = 0;
+  for (int k = 0; k < nch; ++k) {
+    const int64_t r0 = k * per, nr = std::min<int64_t>(per, rows - r0);
+    if (nr <= 0) break;
+    char* dbands = static_cast<char*>(d_bands) + (size_t)sidwt_bands_bytes(p, r0);
+    st = sidwt_analyze(p, static_cast<const char*>(d_rows) + (size_t)r0 * p->N * sb, nr, dbands, p->s_k1);
+    if (st != SIDWT_OK) return st;
+    launches += p->last_launches;
+    e = cudaEventRecord(p->rev[k], p->s_k1);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_k2, p->rev[k], 0);
+    if (e != cudaSuccess) return cuda_status(e);
+    // chunks are serialised on s_k2, so they can share the peak partials buffer
+    char* dcorr = d_corr ? static_cast<char*>(d_corr) + (size_t)sidwt_corr_bytes(p, r0) : nullptr;
+    char* dval = d_val ? static_cast<char*>(d_val) + (size_t)r0 * per_row_out * 8 : nullptr;
+    st = correlate_impl(p, dbands, nr, dcorr, d_lag + r0 * per_row_out, dval, true, p->s_k2);
+    if (st != SIDWT_OK) return st;
+    launches += p->last_launches;
+  }
+  e = cudaEventRecord(ev_done, p->s_k2);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_done, 0);
   p->last_launches = launches;
   return cuda_status(e);

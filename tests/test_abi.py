@@ -58,7 +58,9 @@ def test_plan_validation_without_gpu(native):
     assert L.sidwt_analyze(plan, P(1), 1, P(1), None) == 6      # STATE
     assert L.sidwt_correlate(plan, P(1), 1, P(1), None) == 6
     assert L.sidwt_peaks(plan, P(1), 1, P(1), None, None) == 6
+    assert L.sidwt_run(plan, P(1), 1, P(1), P(1), P(1), None, None) == 6
     assert L.sidwt_analyze(plan, None, 1, P(1), None) == 1      # PARAM
+    assert L.sidwt_run(plan, P(1), 1, None, P(1), P(1), None, None) == 1
     x = (C.c_float * 2)()
     assert L.sidwt_template_load(plan, x, 0, 1) == 2            # LENGTH
     assert L.sidwt_template_load(plan, x, 65, 1) == 2
