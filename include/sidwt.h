@@ -105,6 +105,17 @@ sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t 
  * unknown value or TEMPLATE_TREE with the integer family; STATE after template_load. */
 sidwt_status sidwt_plan_set_orientation(sidwt_plan plan, int orientation);
 
+/* CDF 9/7 plans: the lifting parameter t of the paper's finite-precision family
+ * (PAPER.md:217-219): alpha = (1-2t)/(4(t-1)), beta = -(t-1)^2, gamma = 1/(4t(t-1)),
+ * delta = t^3 - 7/4 t^2 + t, zeta = sqrt(2)/t, used by the template (analysis), the
+ * received (dual) and the synthesis programs alike.  Default t = 5/4 (Table I);
+ * SIDWT_CDF97_T_EXACT gives the irrational CDF 9/7 of the paper's ref. [28].  Call
+ * before sidwt_template_load.  PARAM for a non-9/7 plan or t outside [0.780, 1.852]
+ * (the paper's range) or |t - 1| < 1e-3 (alpha, gamma singular); STATE after
+ * template_load. */
+#define SIDWT_CDF97_T_EXACT 1.2301741049140007
+sidwt_status sidwt_plan_set_lifting_t(sidwt_plan plan, double t);
+
 /* Free the plan and every device buffer it owns.  NULL is accepted. */
 sidwt_status sidwt_plan_destroy(sidwt_plan plan);
 

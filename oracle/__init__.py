@@ -51,6 +51,9 @@ def lib():
         L.oracle_max_threads.restype = i
         L.oracle_approx.argtypes = [i, i, i, i, P, i, i, i, P, i]
         L.oracle_run_paper.argtypes = [i, i, i, i, i, P, i, i, P, P, P, P, i]
+        L.oracle_set_t97.argtypes = [C.c_double]
+        L.oracle_get_t97.restype = C.c_double
+        L.oracle_filter_t97.argtypes = [C.c_double, i, i, C.POINTER(i), C.POINTER(i), P]
         _lib = L
     return _lib
 
@@ -64,6 +67,31 @@ def filt(family: int, role: int, which: int):
     lo, hi = C.c_int(), C.c_int()
     taps = np.zeros(32, dtype=np.float64)
     assert lib().oracle_filter(family, role, which, C.byref(lo), C.byref(hi), _p(taps)) == 0
+    return lo.value, taps[: hi.value - lo.value + 1].copy()
+
+
+class t97:
+    """Context manager: CDF 9/7 free parameter t for every CDF97 call
+    inside the block (default 5/4 = Table I).  Process-wide; not thread-safe."""
+
+    def __init__(self, t: float):
+        self.t = float(t)
+
+    def __enter__(self):
+        self.prev = lib().oracle_get_t97()
+        lib().oracle_set_t97(self.t)
+        return self
+
+    def __exit__(self, *exc):
+        lib().oracle_set_t97(self.prev)
+        return False
+
+
+def filt_t97(t: float, role: int, which: int):
+    """The 9/7 filter of parameter t from the lifting factorisation (not the printed listing)."""
+    lo, hi = C.c_int(), C.c_int()
+    taps = np.zeros(32, dtype=np.float64)
+    assert lib().oracle_filter_t97(float(t), role, which, C.byref(lo), C.byref(hi), _p(taps)) == 0
     return lo.value, taps[: hi.value - lo.value + 1].copy()
 
 

@@ -61,6 +61,92 @@ static double h97(int n) {
     return half[3 - a] * sqrt(2.0);
 }
 
+/* The paper's free-variable 9/7 family, t in [0.780, 1.852]:
+ *   a = (-2t+1)/(4(t-1)), b = -(t-1)^2, g = 1/(4t(t-1)), d = t^3 - 7/4 t^2 + t, x = sqrt2/t.
+ * t = 5/4 is Table I, whose filters are the printed listings above.
+ * For any other t there are no printed filters; they are obtained here by expanding the
+ * lifting factorisations -- the analysis matrix P~(z^-1) and the dual
+ * P^T(z^-1), programs as in DESIGN.md reading R-D3 -- applied to unit
+ * impulses: out[k] = sum_m f[m] x[2k - m] with x = delta_n gives f[2k - n]. */
+static double g_t97 = 1.25;
+
+void oracle_set_t97(double t) { g_t97 = t; }
+double oracle_get_t97(void) { return g_t97; }
+
+static void consts97(double t, double* a, double* b, double* g, double* d, double* x) {
+    *a = (-2.0 * t + 1.0) / (4.0 * (t - 1.0));
+    *b = -(t - 1.0) * (t - 1.0);
+    *g = 1.0 / (4.0 * t * (t - 1.0));
+    *d = t * t * t - 1.75 * t * t + t;
+    *x = sqrt(2.0) / t;
+}
+
+/* Lifting program on pairs k = 0..n-1 (zero outside), e[k] = x[2k], o[k] = x[2k+1].
+ * analysis (R-D3): o += a(e_k + e_{k+1}); e += b(o_k + o_{k-1});
+ *   o += g(e_k + e_{k+1}); e += d(o_k + o_{k-1}); lowpass x e, highpass o / x.
+ * dual (R-D3): e += -a(o_k + o_{k-1}); o += -b(e_k + e_{k+1});
+ *   e += -g(o_k + o_{k-1}); o += -d(e_k + e_{k+1}); lowpass e / x, highpass x o. */
+#define L97N 32
+static void lift97_program(int role, double t, double* e, double* o) {
+    double a, b, g, d, x;
+    consts97(t, &a, &b, &g, &d, &x);
+    double e2[L97N], o2[L97N];
+#define EK(i) (((i) < 0 || (i) >= L97N) ? 0.0 : e[i])
+#define OK(i) (((i) < 0 || (i) >= L97N) ? 0.0 : o[i])
+    if (role == OR_ANALYSIS) {
+        for (int k = 0; k < L97N; k++) o2[k] = o[k] + a * (EK(k) + EK(k + 1));
+        memcpy(o, o2, sizeof o2);
+        for (int k = 0; k < L97N; k++) e2[k] = e[k] + b * (OK(k) + OK(k - 1));
+        memcpy(e, e2, sizeof e2);
+        for (int k = 0; k < L97N; k++) o2[k] = o[k] + g * (EK(k) + EK(k + 1));
+        memcpy(o, o2, sizeof o2);
+        for (int k = 0; k < L97N; k++) e2[k] = e[k] + d * (OK(k) + OK(k - 1));
+        memcpy(e, e2, sizeof e2);
+        for (int k = 0; k < L97N; k++) { e[k] *= x; o[k] /= x; }
+    } else {
+        for (int k = 0; k < L97N; k++) e2[k] = e[k] - a * (OK(k) + OK(k - 1));
+        memcpy(e, e2, sizeof e2);
+        for (int k = 0; k < L97N; k++) o2[k] = o[k] - b * (EK(k) + EK(k + 1));
+        memcpy(o, o2, sizeof o2);
+        for (int k = 0; k < L97N; k++) e2[k] = e[k] - g * (OK(k) + OK(k - 1));
+        memcpy(e, e2, sizeof e2);
+        for (int k = 0; k < L97N; k++) o2[k] = o[k] - d * (EK(k) + EK(k + 1));
+        memcpy(o, o2, sizeof o2);
+        for (int k = 0; k < L97N; k++) { e[k] /= x; o[k] *= x; }
+    }
+#undef EK
+#undef OK
+}
+
+/* Filter f[m], m in [lo, hi], of the t-family by impulse responses (n = 2*16 and 2*16+1). */
+static void filter97_t(double t, int role, int which, filt_t* f) {
+    int lo, hi;
+    if (which == OR_LOWPASS) { lo = (role == OR_ANALYSIS) ? -4 : -3; hi = -lo; }
+    else if (role == OR_ANALYSIS) { lo = -4; hi = 2; }
+    else { lo = -5; hi = 3; }
+    double v[24] = {0};
+    for (int par = 0; par < 2; par++) {
+        const int n = 2 * (L97N / 2) + par;            /* impulse position */
+        double e[L97N] = {0}, o[L97N] = {0};
+        if (par == 0) e[n / 2] = 1.0; else o[n / 2] = 1.0;
+        lift97_program(role, t, e, o);
+        for (int k = 0; k < L97N; k++) {
+            const int m = 2 * k - n;
+            if (m >= lo && m <= hi) v[m - lo] = (which == OR_LOWPASS) ? e[k] : o[k];
+        }
+    }
+    set_filt(f, lo, hi, v);
+}
+
+int oracle_filter_t97(double t, int role, int which, int* lo, int* hi, double* taps) {
+    filt_t f;
+    if (!(t > 0.0) || t == 1.0) return -1;
+    filter97_t(t, role, which, &f);
+    *lo = f.lo; *hi = f.hi;
+    for (int m = f.lo; m <= f.hi; m++) taps[m - f.lo] = f.c[m - f.lo];
+    return 0;
+}
+
 /* Daubechies-4 closed form (textbook, ref [1]/[11]):
  * h0..h3 = (1+sqrt3, 3+sqrt3, 3-sqrt3, 1-sqrt3) / (4 sqrt2). */
 static double hd4(int n) {
@@ -100,6 +186,10 @@ static int get_filter(int family, int role, int which, filt_t* f) {
                 set_filt(f, -3, 1, v);
             }
         }
+        return 0;
+    }
+    if (family == OR_CDF97 && g_t97 != 1.25) {       /* another t: from the lifting factorisation */
+        filter97_t(g_t97, role, which, f);
         return 0;
     }
     if (family == OR_CDF97) {

@@ -34,6 +34,14 @@ enum { OR_PERIODIC = 0, OR_SYMMETRIC = 1 };
 /* Filter f as "coefficient of z^-m", m in [*lo, *hi]; taps[m - *lo]. Returns 0 or -1. */
 int oracle_filter(int family, int role, int which, int* lo, int* hi, double* taps);
 
+/* CDF 9/7 free parameter t (default 5/4 = Table I, printed filters).  A
+ * process-wide setting read by every OR_CDF97 call: set it before a run, not concurrently. */
+void oracle_set_t97(double t);
+double oracle_get_t97(void);
+/* The 9/7 filter of parameter t derived from the lifting factorisation (any t, including
+ * 5/4, where it must reproduce the printed listings).  Returns 0 or -1. */
+int oracle_filter_t97(double t, int role, int which, int* lo, int* hi, double* taps);
+
 /* Support [kmin, kmax] of the template pyramid at level s (1..J): which = lowpass (a_s) / highpass (b_s). */
 int oracle_support(int family, int T, int s, int which, int* kmin, int* kmax);
 

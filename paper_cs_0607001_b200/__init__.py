@@ -10,19 +10,20 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
-from ._native import (SIDWT_CDF97, SIDWT_DAUB4_CAUSAL, SIDWT_EXT_PERIODIC, SIDWT_EXT_SYMMETRIC,  # noqa: F401
+from ._native import (CDF97_T_EXACT, SIDWT_CDF97, SIDWT_DAUB4_CAUSAL, SIDWT_EXT_PERIODIC, SIDWT_EXT_SYMMETRIC,  # noqa: F401
                       SIDWT_LEGALL53, SIDWT_LEGALL53_INT, SIDWT_ORIENT_RECEIVED_TREE, SIDWT_ORIENT_TEMPLATE_TREE,
                       SidwtError)
 
 __all__ = ["Plan", "SidwtError", "SIDWT_LEGALL53", "SIDWT_CDF97", "SIDWT_DAUB4_CAUSAL",
            "SIDWT_LEGALL53_INT", "SIDWT_EXT_PERIODIC", "SIDWT_EXT_SYMMETRIC", "SIDWT_ORIENT_RECEIVED_TREE",
-           "SIDWT_ORIENT_TEMPLATE_TREE"]
+           "SIDWT_ORIENT_TEMPLATE_TREE", "CDF97_T_EXACT"]
 
 
 class Plan:
     """Owns one sidwt_plan.  Device tensors are torch tensors on ``device``."""
 
-    def __init__(self, filter: int, levels: int, N: int, batch: int, ext: int, device="cuda", orientation: int = 0):
+    def __init__(self, filter: int, levels: int, N: int, batch: int, ext: int, device="cuda", orientation: int = 0,
+                 lifting_t: float | None = None):
         import torch  # plumbing only
         self.torch = torch
         self.filter, self.levels, self.N, self.batch, self.ext = filter, levels, N, batch, ext
@@ -31,6 +32,9 @@ class Plan:
         self.orientation = orientation
         if orientation:
             _native.sidwt_plan_set_orientation(self.handle, orientation)
+        self.lifting_t = 1.25 if lifting_t is None else float(lifting_t)
+        if lifting_t is not None:
+            _native.sidwt_plan_set_lifting_t(self.handle, lifting_t)
         self.n_templates = 0
         self.T = 0
 

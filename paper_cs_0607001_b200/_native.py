@@ -23,12 +23,13 @@ SIDWT_LEGALL53, SIDWT_CDF97, SIDWT_DAUB4_CAUSAL, SIDWT_LEGALL53_INT = 0, 1, 2, 3
 SIDWT_EXT_PERIODIC, SIDWT_EXT_SYMMETRIC = 0, 1
 SIDWT_ORIENT_RECEIVED_TREE, SIDWT_ORIENT_TEMPLATE_TREE = 0, 1
 
+CDF97_T_EXACT = 1.2301741049140007   # include/sidwt.h SIDWT_CDF97_T_EXACT (irrational CDF 9/7)
 STATUS = {0: "SIDWT_OK", 1: "SIDWT_ERR_PARAM", 2: "SIDWT_ERR_LENGTH", 3: "SIDWT_ERR_DIMENSION",
           4: "SIDWT_ERR_DEPTH", 5: "SIDWT_ERR_RANGE", 6: "SIDWT_ERR_STATE", 7: "SIDWT_ERR_OOM",
           8: "SIDWT_ERR_CUDA"}
 
 # every symbol include/sidwt.h declares
-EXPORTS = ["sidwt_plan_create", "sidwt_plan_set_orientation", "sidwt_plan_destroy", "sidwt_template_load", "sidwt_analyze",
+EXPORTS = ["sidwt_plan_create", "sidwt_plan_set_orientation", "sidwt_plan_set_lifting_t", "sidwt_plan_destroy", "sidwt_template_load", "sidwt_analyze",
            "sidwt_correlate", "sidwt_peaks", "sidwt_correlate_peaks", "sidwt_run", "sidwt_analyze_correlate", "sidwt_synthesize",
            "sidwt_execute_host", "sidwt_fused_available",
            "sidwt_band_stride", "sidwt_band_offset", "sidwt_bands_bytes", "sidwt_corr_bytes",
@@ -69,6 +70,7 @@ def lib():
         L.sidwt_plan_create.argtypes = [C.POINTER(P), I, I, I64, I64, I]
         L.sidwt_plan_destroy.argtypes = [P]
         L.sidwt_plan_set_orientation.argtypes = [P, I]
+        L.sidwt_plan_set_lifting_t.argtypes = [P, C.c_double]
         L.sidwt_template_load.argtypes = [P, P, I64, I]
         L.sidwt_analyze.argtypes = [P, P, I64, P, P]
         L.sidwt_correlate.argtypes = [P, P, I64, P, P]
@@ -136,6 +138,10 @@ def sidwt_plan_create(filter: int, levels: int, N: int, batch: int, ext: int) ->
 
 def sidwt_plan_set_orientation(plan: int, orientation: int) -> None:
     _check("sidwt_plan_set_orientation", lib().sidwt_plan_set_orientation(plan, orientation))
+
+
+def sidwt_plan_set_lifting_t(plan: int, t: float) -> None:
+    _check("sidwt_plan_set_lifting_t", lib().sidwt_plan_set_lifting_t(plan, float(t)))
 
 
 def sidwt_plan_destroy(plan: int) -> None:

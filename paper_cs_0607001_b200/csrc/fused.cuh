@@ -18,6 +18,7 @@ namespace sidwt {
 struct FusParams {
   int N, J, ext, TT, ntiles, fML, halo_l, lbuf, padl, padr, taps_per_t;
   long long rows;
+  Lift lift;
   int want_corr, want_peaks;
   Term term[kMaxTerms];                // indexed by term (i < J: W_{i+1}, i = J: U_J)
   uint2 ctap[kCTaps];                  // template taps (one template)
@@ -66,8 +67,8 @@ __device__ __forceinline__ void fused_levels(const FusParams& p, typename Dual<F
                                              typename std::conditional<FAM == FI53, int2, float2>::type* D, int tau0) {
   if constexpr (LH < 16) {
     if (LH >= p.J) return;
-    analyze_level<FAM, RV, LH, false>(U0, W0, p.lbuf);
-    analyze_level<FAM, RV, LH, false>(U1, W1, p.lbuf);
+    analyze_level<FAM, RV, LH, false>(U0, W0, p.lbuf, p.lift);
+    analyze_level<FAM, RV, LH, false>(U1, W1, p.lbuf, p.lift);
     fused_term<FAM, Q>(p, LH, W0, W1, D, tau0);                // D_{LH+1} from W_{LH+1}
     // the next level reads U only and writes W after its first barrier
     fused_levels<FAM, RV, LH + 1, Q>(p, U0, W0, U1, W1, D, tau0);

@@ -54,6 +54,7 @@ struct PyrParams {
   int npad[kMaxTerms];                                  // residue stride of a term (paper orientation)
   int scratch_len;                                      // per-thread scratch length (doubles)
   int nres;                                             // 1, or 2^J residues (paper orientation)
+  Lift64 lift;                                          // 9/7 analysis constants
 };
 
 template <typename V>
@@ -62,7 +63,7 @@ __device__ __forceinline__ V getz(const V* a, long lo, long hi, long n) {
 }
 
 template <typename V>
-__device__ void analysis_level(int fam, const V* cur, long lo, long hi, V* e, V* o, long klo, long khi) {
+__device__ void analysis_level(int fam, const Lift64& L, const V* cur, long lo, long hi, V* e, V* o, long klo, long khi) {
   // fill e/o over [klo, khi]; conv A: (x[2k], x[2k+1]); causal D4 (R-D1): (x[2k], x[2k-1])
   for (long k = klo; k <= khi; ++k) {
     e[k - klo] = getz(cur, lo, hi, 2 * k);
@@ -76,11 +77,11 @@ __device__ void analysis_level(int fam, const V* cur, long lo, long hi, V* e, V*
     for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(0.25) * (O(i) + O(i - 1));
     for (long i = 0; i < n; ++i) o[i] = V(0.5) * o[i];
   } else if (fam == F97) {      // PAPER.md:238, reading R-D3
-    for (long i = 0; i < n; ++i) o[i] = o[i] + V(kAlpha) * (E(i) + E(i + 1));
-    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(kBeta) * (O(i) + O(i - 1));
-    for (long i = 0; i < n; ++i) o[i] = o[i] + V(kGamma) * (E(i) + E(i + 1));
-    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(kDelta) * (O(i) + O(i - 1));
-    for (long i = 0; i < n; ++i) { e[i] = V(kZeta) * e[i]; o[i] = o[i] / V(kZeta); }
+    for (long i = 0; i < n; ++i) o[i] = o[i] + V(L.a) * (E(i) + E(i + 1));
+    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(L.b) * (O(i) + O(i - 1));
+    for (long i = 0; i < n; ++i) o[i] = o[i] + V(L.g) * (E(i) + E(i + 1));
+    for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(L.d) * (O(i) + O(i - 1));
+    for (long i = 0; i < n; ++i) { e[i] = V(L.z) * e[i]; o[i] = o[i] / V(L.z); }
   } else if (fam == FD4) {      // eq. (17)
     for (long i = 0; i < n; ++i) o[i] = o[i] - V(kSqrt3) * e[i];
     for (long i = n - 1; i >= 0; --i) e[i] = e[i] + V(kD4c1) * O(i) + V(kD4c2) * O(i - 1);
@@ -134,7 +135,7 @@ __global__ void k_template_pyramid(const void* __restrict__ x, void* __restrict_
       const long alo = cl_div2(lo + sp.lLo), ahi = fl_div2(hi + sp.lHi);
       const long blo = cl_div2(lo + sp.hLo), bhi = fl_div2(hi + sp.hHi);
       const long klo = (alo < blo ? alo : blo) - 2, khi = (ahi > bhi ? ahi : bhi) + 2;
-      analysis_level<double>(p.fam, cur, lo, hi, e, o, klo, khi);
+      analysis_level<double>(p.fam, p.lift, cur, lo, hi, e, o, klo, khi);
       const int ti = s - 1;
       const int sl = slot(ti);
       if (sl >= 0)
@@ -191,11 +192,12 @@ struct AnaParams {
   int tile_len, ntiles, halo_l, lbuf;
   int padl, padr;
   long long rows;
+  Lift lift;
 };
 
 template <int FAM, int RV, int LH, bool BULK = true>
 __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict__ U, typename Dual<FAM>::T* __restrict__ Wst,
-                                              int lbuf) {
+                                              int lbuf, const Lift& L) {
   typedef typename Dual<FAM>::T T;
   constexpr int HL = Dual<FAM>::HL, HR = Dual<FAM>::HR, WIN = RV + HL + HR;
   constexpr int h = 1 << LH;
@@ -211,7 +213,7 @@ __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict_
     T v[WIN];
 #pragma unroll
     for (int i = 0; i < WIN; ++i) v[i] = src[i * h];
-    Dual<FAM>::template run<RV>(v, c, d);
+    Dual<FAM>::template run<RV>(v, c, d, L);
   }
   if (BULK && threadIdx.x == 0 && LH > 0) bulk_wait_read_all();   // staging free again
   __syncthreads();
@@ -230,15 +232,16 @@ __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict_
 // followed by the bulk store of its detail plane.
 template <int FAM, int RV, int LH>
 __device__ __forceinline__ void analyze_levels(int J, typename Dual<FAM>::T* U, typename Dual<FAM>::T* Wst, int lbuf,
-                                               typename Dual<FAM>::T* plane0, size_t band_step, int halo_l, int out_len) {
+                                               typename Dual<FAM>::T* plane0, size_t band_step, int halo_l, int out_len,
+                                               const Lift& L) {
   if constexpr (LH < 16) {
     if (LH >= J) return;
-    analyze_level<FAM, RV, LH>(U, Wst, lbuf);
+    analyze_level<FAM, RV, LH>(U, Wst, lbuf, L);
     if (threadIdx.x == 0) {
       bulk_store_s2g(plane0 + (size_t)LH * band_step, Wst + halo_l, (uint32_t)(out_len * sizeof(typename Dual<FAM>::T)));
       bulk_commit();
     }
-    analyze_levels<FAM, RV, LH + 1>(J, U, Wst, lbuf, plane0, band_step, halo_l, out_len);
+    analyze_levels<FAM, RV, LH + 1>(J, U, Wst, lbuf, plane0, band_step, halo_l, out_len, L);
   }
 }
 
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
   T* plane0 = static_cast<T*>(bands) + ((size_t)row * (p.J + 1) * 2 + comp) * p.stride + tstart;
   const size_t band_step = (size_t)2 * p.stride;
 
-  analyze_levels<FAM, RV, 0>(p.J, U, Wst, p.lbuf, plane0, band_step, p.halo_l, out_len);
+  analyze_levels<FAM, RV, 0>(p.J, U, Wst, p.lbuf, plane0, band_step, p.halo_l, out_len, p.lift);
   if (threadIdx.x == 0) {
     bulk_store_s2g(plane0 + (size_t)p.J * band_step, U + p.halo_l, (uint32_t)(out_len * sizeof(T)));
     bulk_commit();
@@ -330,6 +333,7 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
 struct SynParams {
   int N, J, ext, stride, ML, level, TL, ntiles, halo_l, halo_r, lbuf;
   long long rows;
+  Lift lift;
 };
 
 template <int FAM>
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(256) k_synthesize(const void* __restrict__ ban
       T c[W], d[W];
 #pragma unroll
       for (int m = 0; m < W; ++m) { c[m] = A[u + (m - SL) * st]; d[m] = B[u + (m - SL) * st]; }
-      C[u] = Inverse<FAM>::e(c, d);
+      C[u] = Inverse<FAM>::e(c, d, p.lift);
     }
     __syncthreads();
     T* tmp = A; A = C; C = tmp;

@@ -17,6 +17,23 @@ enum Family { F53 = 0, F97 = 1, FD4 = 2, FI53 = 3 };
 // Table I, t = 5/4.
 constexpr double kAlpha = -1.5, kBeta = -0.0625, kGamma = 0.8, kDelta = 0.46875;
 constexpr double kZeta = 1.1313708498984760390;      // 4 sqrt(2) / 5
+
+// 9/7 lifting constants as kernel parameters.  The paper's free-variable family
+// (the finite-precision 9/7 of its ref. [10]):
+//   alpha = (1 - 2t) / (4 (t - 1)), beta = -(t - 1)^2, gamma = 1 / (4 t (t - 1)),
+//   delta = t^3 - 7/4 t^2 + t, zeta = sqrt(2) / t,
+// with t = 5/4 giving Table I and t = 1.2301741... the irrational CDF 9/7 of ref. [28].
+// The other families ignore them.
+struct Lift64 { double a, b, g, d, z; };
+struct Lift { float a, b, g, d, z, iz; };
+__host__ inline Lift64 lift97_t(double t) {
+  if (t == 1.25) return {kAlpha, kBeta, kGamma, kDelta, kZeta};
+  return {(1.0 - 2.0 * t) / (4.0 * (t - 1.0)), -(t - 1.0) * (t - 1.0), 1.0 / (4.0 * t * (t - 1.0)),
+          t * t * t - 1.75 * t * t + t, 1.4142135623730950488 / t};
+}
+__host__ inline Lift lift_f32(const Lift64& k) {
+  return {(float)k.a, (float)k.b, (float)k.g, (float)k.d, (float)k.z, (float)(1.0 / k.z)};
+}
 // eq. (17)
 constexpr double kSqrt3 = 1.7320508075688772935;
 constexpr double kD4c1 = 0.43301270189221932338;     // sqrt3 / 4
@@ -36,7 +53,7 @@ template <> struct Dual<F53> {
   typedef float T;
   static constexpr int HL = 1, HR = 3;
   template <int RV>
-  __device__ __forceinline__ static void run(const float (&v)[RV + HL + HR], float (&c)[RV], float (&d)[RV]) {
+  __device__ __forceinline__ static void run(const float (&v)[RV + HL + HR], float (&c)[RV], float (&d)[RV], const Lift& L) {
     float e1[RV + 2];
 #pragma unroll
     for (int a = 0; a < RV + 2; ++a) e1[a] = fmaf(0.5f, v[a] + v[a + 2], v[a + 1]);
@@ -55,8 +72,8 @@ template <> struct Dual<F97> {
   typedef float T;
   static constexpr int HL = 3, HR = 5;
   template <int RV>
-  __device__ __forceinline__ static void run(const float (&v)[RV + HL + HR], float (&c)[RV], float (&d)[RV]) {
-    const float na = (float)-kAlpha, nb = (float)-kBeta, ng = (float)-kGamma, nd = (float)-kDelta;
+  __device__ __forceinline__ static void run(const float (&v)[RV + HL + HR], float (&c)[RV], float (&d)[RV], const Lift& L) {
+    const float na = -L.a, nb = -L.b, ng = -L.g, nd = -L.d;
     float e1[RV + 6], o1[RV + 4], e2[RV + 2];
 #pragma unroll
     for (int a = 0; a < RV + 6; ++a) e1[a] = fmaf(na, v[a] + v[a + 2], v[a + 1]);      // j = j0-2+a
@@ -67,8 +84,8 @@ template <> struct Dual<F97> {
 #pragma unroll
     for (int b = 0; b < RV; ++b) {
       const float o2 = fmaf(nd, e2[b] + e2[b + 2], o1[b + 2]);
-      c[b] = e2[b] * (float)(1.0 / kZeta);
-      d[b] = o2 * (float)kZeta;
+      c[b] = e2[b] * L.iz;
+      d[b] = o2 * L.z;
     }
   }
 };
@@ -79,7 +96,7 @@ template <> struct Dual<FD4> {
   typedef float T;
   static constexpr int HL = 3, HR = 0;
   template <int RV>
-  __device__ __forceinline__ static void run(const float (&v)[RV + HL + HR], float (&c)[RV], float (&d)[RV]) {
+  __device__ __forceinline__ static void run(const float (&v)[RV + HL + HR], float (&c)[RV], float (&d)[RV], const Lift& L) {
     float o1[RV + 2];
 #pragma unroll
     for (int a = 0; a < RV + 2; ++a) o1[a] = fmaf(-(float)kSqrt3, v[a + 1], v[a]);      // j = j0-2+a
@@ -98,7 +115,7 @@ template <> struct Dual<FI53> {
   typedef int T;
   static constexpr int HL = 1, HR = 3;
   template <int RV>
-  __device__ __forceinline__ static void run(const int (&v)[RV + HL + HR], int (&c)[RV], int (&d)[RV]) {
+  __device__ __forceinline__ static void run(const int (&v)[RV + HL + HR], int (&c)[RV], int (&d)[RV], const Lift&) {
     int e1[RV + 2];
 #pragma unroll
     for (int a = 0; a < RV + 2; ++a) e1[a] = v[a + 1] + ((v[a] + v[a + 2]) >> 1);
@@ -122,7 +139,7 @@ template <int FAM> struct Inverse;
 template <> struct Inverse<F53> {
   typedef float T;
   static constexpr int SL = 1, SR = 1;
-  __device__ __forceinline__ static float e(const float (&c)[3], const float (&d)[3]) {
+  __device__ __forceinline__ static float e(const float (&c)[3], const float (&d)[3], const Lift&) {
     const float ok = fmaf(0.5f, d[1], 0.25f * (c[1] + c[2]));
     const float om = fmaf(0.5f, d[0], 0.25f * (c[0] + c[1]));
     return fmaf(-0.5f, ok + om, c[1]);
@@ -134,20 +151,20 @@ template <> struct Inverse<F53> {
 template <> struct Inverse<F97> {
   typedef float T;
   static constexpr int SL = 2, SR = 2;
-  __device__ __forceinline__ static float e(const float (&c)[5], const float (&d)[5]) {
-    const float z = (float)kZeta, iz = (float)(1.0 / kZeta);
+  __device__ __forceinline__ static float e(const float (&c)[5], const float (&d)[5], const Lift& L) {
+    const float z = L.z, iz = L.iz;
     float e4[5], o4[4], o3[4], e2[3], o1[2];
 #pragma unroll
     for (int i = 0; i < 5; ++i) e4[i] = z * c[i];          // m = i - 2
 #pragma unroll
     for (int i = 0; i < 4; ++i) o4[i] = iz * d[i];         // m = i - 2
 #pragma unroll
-    for (int i = 0; i < 4; ++i) o3[i] = fmaf((float)kDelta, e4[i] + e4[i + 1], o4[i]);   // m = i - 2
+    for (int i = 0; i < 4; ++i) o3[i] = fmaf(L.d, e4[i] + e4[i + 1], o4[i]);   // m = i - 2
 #pragma unroll
-    for (int i = 0; i < 3; ++i) e2[i] = fmaf((float)kGamma, o3[i + 1] + o3[i], e4[i + 1]);  // m = i - 1
+    for (int i = 0; i < 3; ++i) e2[i] = fmaf(L.g, o3[i + 1] + o3[i], e4[i + 1]);  // m = i - 1
 #pragma unroll
-    for (int i = 0; i < 2; ++i) o1[i] = fmaf((float)kBeta, e2[i] + e2[i + 1], o3[i + 1]);   // m = i - 1
-    return fmaf((float)kAlpha, o1[1] + o1[0], e2[1]);
+    for (int i = 0; i < 2; ++i) o1[i] = fmaf(L.b, e2[i] + e2[i + 1], o3[i + 1]);   // m = i - 1
+    return fmaf(L.a, o1[1] + o1[0], e2[1]);
   }
 };
 
@@ -156,7 +173,7 @@ template <> struct Inverse<F97> {
 template <> struct Inverse<FD4> {
   typedef float T;
   static constexpr int SL = 0, SR = 1;
-  __device__ __forceinline__ static float e(const float (&c)[2], const float (&d)[2]) {
+  __device__ __forceinline__ static float e(const float (&c)[2], const float (&d)[2], const Lift&) {
     const float ik1 = (float)(1.0 / kD4K1), ik2 = (float)(1.0 / kD4K2);
     const float e1k = ik1 * c[0], e1n = ik1 * c[1];
     const float o1k = fmaf(ik2, d[1], -e1n), o1m = fmaf(ik2, d[0], -e1k);
@@ -169,7 +186,7 @@ template <> struct Inverse<FD4> {
 template <> struct Inverse<FI53> {
   typedef int T;
   static constexpr int SL = 1, SR = 1;
-  __device__ __forceinline__ static int e(const int (&c)[3], const int (&d)[3]) {
+  __device__ __forceinline__ static int e(const int (&c)[3], const int (&d)[3], const Lift&) {
     const int ok = d[1] + ((c[1] + c[2] + 2) >> 2);
     const int om = d[0] + ((c[0] + c[1] + 2) >> 2);
     return c[1] - ((ok + om) >> 1);

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -66,6 +67,7 @@ struct sidwt_plan_s {
   bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
   bool real_taps = false;        // every template tap has a zero imaginary part
   int run_chunks = 1;            // sidwt_run default chunk count
+  double t97 = 1.25;             // 9/7 lifting parameter t (Table I)
   // fused analyze -> correlate -> peaks (single template)
   bool fused = false;
   FusParams* fus = nullptr;      // host copy (large: carries the taps)
@@ -133,6 +135,14 @@ sidwt_status sidwt_plan_destroy(sidwt_plan plan) {
   if (!plan) return SIDWT_OK;
   free_ws(plan);
   delete plan;
+  return SIDWT_OK;
+}
+
+sidwt_status sidwt_plan_set_lifting_t(sidwt_plan p, double t) {
+  if (!p || p->fam != F97) return SIDWT_ERR_PARAM;
+  if (!(t >= 0.780 && t <= 1.852) || std::fabs(t - 1.0) < 1e-3) return SIDWT_ERR_PARAM;
+  if (p->loaded) return SIDWT_ERR_STATE;
+  p->t97 = t;
   return SIDWT_OK;
 }
 
@@ -233,6 +243,7 @@ static void configure(sidwt_plan_s* p) {
     if ((lbuf <= lbuf_target && threads <= 512) || tile_len <= 32) break;
   }
   ntiles = cdiv(p->stride, tile_len);
+  p->ana.lift = lift_f32(lift97_t(p->t97));
   p->ana.N = (int)p->N; p->ana.J = J; p->ana.ext = p->ext; p->ana.stride = (int)p->stride; p->ana.ML = ML;
   p->ana.tile_len = (int)tile_len; p->ana.ntiles = (int)ntiles; p->ana.halo_l = (int)halo_l; p->ana.lbuf = (int)lbuf;
   // pads absorbing the clamp-free window reads / run writes past the buffer ends (top level)
@@ -336,6 +347,7 @@ static void configure_fused(sidwt_plan_s* p) {
   if (!p->fus) p->fus = new (std::nothrow) FusParams();
   if (!p->fus) return;
   FusParams& f = *p->fus;
+  f.lift = lift_f32(lift97_t(p->t97));
   const int J = p->J;
   int fML = 0, fMR = 0;
   for (int i = 0; i <= J; ++i) {
@@ -402,6 +414,7 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   }
   pp.scratch_len = (int)T + 64;
   pp.nres = p->paper ? (1 << p->J) : 1;
+  pp.lift = lift97_t(p->t97);
   void* d_x = nullptr;
   double* d_scr = nullptr;
   cudaError_t e = cudaMalloc(&p->d_taps, tab_bytes);
@@ -696,6 +709,7 @@ static cudaError_t launch_synthesize(const sidwt_plan_s* p, const void* bands, i
   int sl = 0, sr = 0;
   inverse_reach(p->fam, sl, sr);
   SynParams q{};
+  q.lift = lift_f32(lift97_t(p->t97));
   q.N = (int)p->N; q.J = p->J; q.ext = p->ext; q.stride = (int)p->stride; q.ML = p->ML; q.level = level;
   q.TL = (int)std::min<int64_t>(p->N, 2048);
   q.ntiles = (int)cdiv(p->N, q.TL);

@@ -59,6 +59,7 @@ def test_plan_validation_without_gpu(native):
     assert L.sidwt_correlate(plan, P(1), 1, P(1), None) == 6
     assert L.sidwt_peaks(plan, P(1), 1, P(1), None, None) == 6
     assert L.sidwt_run(plan, P(1), 1, P(1), P(1), P(1), None, None) == 6
+    assert L.sidwt_plan_set_lifting_t(plan, 1.3) == 1                # PARAM: not a 9/7 plan
     assert L.sidwt_analyze(plan, None, 1, P(1), None) == 1      # PARAM
     assert L.sidwt_run(plan, P(1), 1, None, P(1), P(1), None, None) == 1
     x = (C.c_float * 2)()

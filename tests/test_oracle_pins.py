@@ -619,3 +619,112 @@ def test_paper_orientation_dense_matrices():
             ks = np.arange(ax.shape[0]) - off // (2 ** s)
             val = np.sum(np.conj(ax) * cy[np.mod(ks, N >> s)])
             assert abs(val - rp["corr"][0, 0, s, tau]) < 1e-10, (s, tau)
+
+
+# ---------------------------------------------------------------- the free-t 9/7 family
+
+T_EXACT = 1.2301741049140007        # include/sidwt.h SIDWT_CDF97_T_EXACT
+
+
+def _cdf97_spectral():
+    """The irrational CDF 9/7 lowpass pair (ref. [28] of the paper) built from scratch by
+    spectral factorisation, independent of any lifting: |H|^2-type product
+    cos^8(w/2) P(sin^2(w/2)) with P(y) = sum_{k<4} C(3+k, k) y^k; the complex root pair of P
+    goes to the 9-tap filter, the real root to the 7-tap one; both normalised to DC gain sqrt2."""
+    r = np.roots([math.comb(3 + k, k) for k in range(3, -1, -1)])
+    y0 = r[np.argmin(abs(r.imag))].real
+    yc = r[np.argmax(r.imag)]
+    Y = np.array([-1, 2, -1]) / 4.0                       # sin^2(w/2) as a Laurent polynomial
+    cos4 = np.convolve([1, 2, 1], [1, 2, 1]) / 16.0       # cos^4(w/2)
+    one = np.array([0, 1.0, 0])
+    f9 = np.convolve(cos4, np.real(np.convolve(one - Y / yc, one - Y / np.conj(yc))))
+    f7 = np.convolve(cos4, one - Y / y0)
+    f9, f7 = f9[np.abs(f9) > 1e-15], f7[np.abs(f7) > 1e-15]
+    return f9 * math.sqrt(2) / f9.sum(), f7 * math.sqrt(2) / f7.sum()
+
+
+def test_t97_lifting_expansion_reproduces_printed_filters():
+    """At t = 5/4 the oracle's expansion of the lifting factorisations
+    gives the printed 9/7 listings and their eq. (7) highpass filters."""
+    for role in (O.ANALYSIS, O.DUAL):
+        for which in (O.LOWPASS, O.HIGHPASS):
+            lo_p, printed = O.filt(O.CDF97, role, which)
+            lo_t, derived = O.filt_t97(1.25, role, which)
+            assert lo_p == lo_t
+            np.testing.assert_allclose(derived, printed, atol=1e-15)
+
+
+def test_t97_exact_cdf_equals_spectral_factorisation():
+    """At t = t* (alpha(t*) = the CDF value) the free-t family is the irrational CDF 9/7
+    filterbank: both lowpass filters equal the spectral factorisation,
+    and both highpass filters have four vanishing moments -- Table I's dual
+    highpass has only two."""
+    f9, f7 = _cdf97_spectral()
+    lo, a = O.filt_t97(T_EXACT, O.ANALYSIS, O.LOWPASS)
+    assert lo == -4 and len(a) == 9
+    np.testing.assert_allclose(a, f9, atol=1e-14)
+    lo, d = O.filt_t97(T_EXACT, O.DUAL, O.LOWPASS)
+    assert lo == -3 and len(d) == 7
+    np.testing.assert_allclose(d, f7, atol=1e-14)
+    for role in (O.ANALYSIS, O.DUAL):
+        lo, g = O.filt_t97(T_EXACT, role, O.HIGHPASS)
+        m = np.arange(lo, lo + len(g), dtype=np.float64)
+        for p in range(4):
+            assert abs(np.sum(g * m ** p)) < 1e-12, (role, p)
+        assert abs(np.sum(g * m ** 4)) > 1.0
+    lo, g = O.filt_t97(1.25, O.DUAL, O.HIGHPASS)
+    m = np.arange(lo, lo + len(g), dtype=np.float64)
+    assert abs(np.sum(g * m ** 2)) > 0.1
+
+
+@pytest.mark.parametrize("t", (0.8, T_EXACT, 1.6, 1.85))
+def test_t97_biorthogonal_and_inner_product(t):
+    """Any t of the family is a biorthogonal pair: dual^T analysis = I (eq. (11)/(13)) and
+    the one-level inner-product identity <x, y> = <a, c> + <b, d> (eq. (4)/(15))."""
+    with O.t97(t):
+        for P in (8, 16, 32):
+            Ma = _dense(O.CDF97, O.ANALYSIS, P)
+            Md = _dense(O.CDF97, O.DUAL, P)
+            np.testing.assert_allclose(Md.T @ Ma, np.eye(P), atol=1e-12)
+            x = RNG.normal(size=P) + 1j * RNG.normal(size=P)
+            y = RNG.normal(size=P) + 1j * RNG.normal(size=P)
+            a, b = O.mallat_level(O.CDF97, O.ANALYSIS, x)
+            c, d = O.mallat_level(O.CDF97, O.DUAL, y)
+            assert abs(np.vdot(x, y) - np.vdot(a, c) - np.vdot(b, d)) < 1e-11 * (1 + abs(np.vdot(x, y)))
+        # the setting is scoped
+    lo, f = O.filt(O.CDF97, O.ANALYSIS, O.LOWPASS)
+    np.testing.assert_allclose(f, O.filt_t97(1.25, O.ANALYSIS, O.LOWPASS)[1], atol=1e-15)
+
+
+@pytest.mark.parametrize("ext", (O.PERIODIC, O.SYMMETRIC))
+def test_t97_full_path_pins(ext):
+    """Exact CDF 9/7 through the whole oracle: corr_0 is the textbook correlation (P9) and
+    the telescoped eq. (4) form equals the approximation-domain form (P10) at every scale."""
+    N, J, T = 64, 4, 23
+    y = RNG.normal(size=N) + 1j * RNG.normal(size=N)
+    x = RNG.normal(size=T) + 1j * RNG.normal(size=T)
+    with O.t97(T_EXACT):
+        r = O.run(O.CDF97, J, ext, N, y[None], x[None])
+        pyr = O.template_pyramid(O.CDF97, J, x)
+        lo = min(min(2 ** (i + 1) * k for i, (k, _) in enumerate(pyr[:-1])), 2 ** J * pyr[-1][0])
+        hi = max(max(2 ** (i + 1) * (k + len(c) - 1) for i, (k, c) in enumerate(pyr[:-1])),
+                 2 ** J * (pyr[-1][0] + len(pyr[-1][1]) - 1))
+        rb = O.run(O.CDF97, J, ext, N, y[None], x[None], p_lo=lo, p_hi=N + hi + 1)
+    ref = np.array([sum(np.conj(x[n]) * _extend(y, ext, np.array([n + tau]))[0] for n in range(T))
+                    for tau in range(N)])
+    np.testing.assert_allclose(r["corr"][0, 0, 0], ref, atol=1e-12)
+    B = rb["bands"][0]
+    corr = np.zeros(N, np.complex128)
+    for i in range(J, -1, -1):
+        k0, c = pyr[i]
+        lev = i + 1 if i < J else J
+        for j, cc in enumerate(c):
+            corr = corr + np.conj(cc) * B[i, np.arange(N) + 2 ** lev * (k0 + j) - lo]
+        s = i if i < J else J
+        if i == J:
+            np.testing.assert_allclose(r["corr"][0, 0, J], corr, atol=1e-10)
+        else:
+            np.testing.assert_allclose(r["corr"][0, 0, s], corr, atol=1e-10)
+    # and it differs from Table I away from s = 0
+    r125 = O.run(O.CDF97, J, ext, N, y[None], x[None])
+    assert np.max(np.abs(r125["corr"][0, 0, 2] - r["corr"][0, 0, 2])) > 1e-6
