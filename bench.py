@@ -357,12 +357,13 @@ def main():
 
     pk = load_peaks()
     alg = algorithmic(cfg, plan)
-    tc = plan.uses_tensor_cores()
+    tc_path = plan.tensor_core_path()            # 0 SIMT, 1 template bank, 2 single template
+    tc = tc_path > 0
     k1_gbs = R * alg["k1_bytes"] / (k1_ms * 1e-3) / 1e9
     k2_tflops = R * alg["k2_flops"] / (k2_ms * 1e-3) / 1e12
     k2_gbs = R * alg["k2_bytes"] / (k2_ms * 1e-3) / 1e9
     fp32_peak = fp32_peak_tflops(pk["sm_mhz"])
-    k2_kernel = "k_correlate_tc" if tc else "k_correlate"
+    k2_kernel = ("k_correlate", "k_correlate_tc", "k_correlate_tcs")[tc_path]
     if tc:
         # tensor pipe: the algorithmic complex MACs run as 3 bf16 products (split precision);
         # peak = measured sustained cuBLAS bf16 (the kernel runs inside a long power-capped step)
@@ -379,7 +380,7 @@ def main():
     stages = {
         "analyze": {"kernel": "k_analyze", "ms": k1_ms, "bound": "hbm", "achieved": k1_gbs, "peak": pk["hbm"],
                     "unit": "GB/s", "frac": k1_gbs / pk["hbm"], "bytes_per_row": alg["k1_bytes"]},
-        "correlate_peaks": {"kernel": k2_kernel + "+k_peaks_finalize", "ms": k2_ms,
+        "correlate_peaks": {"kernel": k2_kernel + ("" if tc_path == 2 else "+k_peaks_finalize"), "ms": k2_ms,
                             comp_key: comp,
                             "hbm": {"achieved": k2_gbs, "peak": pk["hbm"], "unit": "GB/s",
                                     "frac": k2_gbs / pk["hbm"], "bytes_per_row": alg["k2_bytes"]}},

@@ -149,7 +149,13 @@ sidwt_status sidwt_analyze(sidwt_plan plan, const void* d_rows, int64_t rows, vo
  * into bf16 hi + lo, three products (hi.hi + hi.lo + lo.hi) accumulated in fp32;
  * error ~1e-5 of the peak |corr| (the fp32 SIMT kernel: ~1e-7).  Environment
  * SIDWT_TC=0 disables this path, SIDWT_TC=1 forces it for any bank size; read at
- * template_load.  Otherwise the per-lag FP32 (INT32) SIMT kernel runs. */
+ * template_load.  A single complex template with a long finest term (>= 128 taps; float
+ * family, symmetric extension, N/64 in [16, 256] with the tiles fitting in shared memory,
+ * 2^levels <= N/64) runs on the tensor
+ * cores as a Toeplitz-block GEMM (the template's Toeplitz matrix against the band
+ * gathered per residue class; same split precision); SIDWT_TCS=0 disables it, SIDWT_TCS=1
+ * forces it for any single template that fits.  Otherwise the per-lag FP32 (INT32) SIMT
+ * kernel runs. */
 sidwt_status sidwt_correlate(sidwt_plan plan, const void* d_bands, int64_t rows, void* d_corr,
                              void* stream);
 
@@ -228,8 +234,9 @@ int64_t sidwt_corr_bytes(sidwt_plan plan, int64_t rows);
  * be NULL to query only.  Returns the number of taps per template or -1. */
 int64_t sidwt_template_taps(sidwt_plan plan, void* host_taps, int32_t* kmin, int32_t* count);
 
-/* 1 if sidwt_correlate* of this plan run on the tensor cores (bank path), 0 if on the
- * SIMT pipes, -1 before template_load. */
+/* 1 if sidwt_correlate* of this plan run on the tensor cores as a template bank, 2 if
+ * as a single-template Toeplitz-block GEMM, 0 if on the SIMT pipes, -1 before
+ * template_load. */
 int sidwt_uses_tensor_cores(sidwt_plan plan);
 
 /* 1 if every tap of the loaded template bank is real (zero imaginary part, e.g. a Barker

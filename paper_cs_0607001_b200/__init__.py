@@ -184,7 +184,12 @@ class Plan:
         return _native.sidwt_template_is_real(self.handle) == 1
 
     def uses_tensor_cores(self) -> bool:
-        return _native.sidwt_uses_tensor_cores(self.handle) == 1
+        """True when the correlation runs on the tensor cores (template bank or single template)."""
+        return _native.sidwt_uses_tensor_cores(self.handle) > 0
+
+    def tensor_core_path(self) -> int:
+        """0: SIMT correlation; 1: template-bank tcgen05 kernel; 2: single-template tcgen05 kernel."""
+        return _native.sidwt_uses_tensor_cores(self.handle)
 
     def last_launches(self) -> int:
         return _native.sidwt_last_launches(self.handle)

@@ -13,7 +13,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libsidwt.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sidwt.cu", "kernels.cuh", "lifting.cuh", "corr_tc.cuh", "fused.cuh")] + [
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sidwt.cu", "kernels.cuh", "lifting.cuh", "corr_tc.cuh", "corr_tcs.cuh", "fused.cuh")] + [
     os.path.join(ROOT, "include", "sidwt.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

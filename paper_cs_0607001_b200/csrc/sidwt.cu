@@ -16,6 +16,7 @@
 #include "../../include/sidwt.h"
 #include "kernels.cuh"
 #include "corr_tc.cuh"
+#include "corr_tcs.cuh"
 #include "fused.cuh"
 
 using namespace sidwt;
@@ -79,6 +80,11 @@ struct sidwt_plan_s {
   TcParams tcp{};
   void* d_img = nullptr;
   size_t tc_smem = 0;
+  bool tcs = false;                  // single-template tensor-core correlation (corr_tcs.cuh)
+  TcsParams tcsp{};
+  void* d_tcs_img = nullptr;
+  size_t tcs_smem = 0;
+  int tcs_total_ksteps = 0;
 };
 
 static bool is_int(const sidwt_plan_s* p) { return p->fam == SIDWT_LEGALL53_INT; }
@@ -117,7 +123,8 @@ sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t 
 }
 
 static void free_ws(sidwt_plan_s* p) {
-  void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val, &p->d_img};
+  void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val, &p->d_img,
+                   &p->d_tcs_img};
   for (void** b : bufs) { if (*b) cudaFree(*b); *b = nullptr; }
   for (cudaEvent_t& ev : p->ev) { if (ev) cudaEventDestroy(ev); ev = nullptr; }
   if (p->d_fpartials) { cudaFree(p->d_fpartials); p->d_fpartials = nullptr; p->fpartials_bytes = 0; }
@@ -165,7 +172,7 @@ int64_t sidwt_corr_bytes(sidwt_plan p, int64_t rows) {
   return rows * p->n_t * (p->J + 1) * p->N * 8;
 }
 int sidwt_last_launches(sidwt_plan p) { return p ? p->last_launches : 0; }
-int sidwt_uses_tensor_cores(sidwt_plan p) { return (p && p->loaded) ? (p->tc ? 1 : 0) : -1; }
+int sidwt_uses_tensor_cores(sidwt_plan p) { return (p && p->loaded) ? (p->tc ? 1 : (p->tcs ? 2 : 0)) : -1; }
 int sidwt_template_is_real(sidwt_plan p) { return (p && p->loaded) ? (p->real_taps ? 1 : 0) : -1; }
 
 // ---------------------------------------------------------------------------
@@ -338,6 +345,55 @@ static void configure_tc(sidwt_plan_s* p) {
   p->tc = true;
 }
 
+// Single-template tensor-core path (corr_tcs.cuh): float families, one template,
+// symmetric extension, N / 64 columns in [16, 256] (multiple of 16), every residue class
+// at least one 64-lag block long (2^J <= N / 64).  SIDWT_TCS=0 disables it.
+static void configure_tcs(sidwt_plan_s* p) {
+  p->tcs = false;
+  const char* env = std::getenv("SIDWT_TCS");
+  if (env && env[0] == '0') return;
+  // default: complex templates with a long finest term (measured: C3 correlation 14.9 -> 9.4 ms);
+  // real / short templates stay on the SIMT kernel (C2: 0.48 ms SIMT vs 1.2 ms here)
+  if (!(env && env[0] == '1') && (p->real_taps || p->cnt[0] < 128)) return;
+  if (p->paper || is_int(p) || p->n_t != 1 || p->ext != SIDWT_EXT_SYMMETRIC || p->tc) return;
+  if (p->N % 64 != 0) return;
+  const int ncols = (int)(p->N / 64);
+  if (ncols < 16 || ncols > 256 || ncols % 16 != 0 || (1LL << p->J) > ncols) return;
+  TcsParams& t = p->tcsp;
+  t = TcsParams{};
+  t.N = (int)p->N; t.J = p->J; t.stride = (int)p->stride; t.ML = p->ML; t.ncols = ncols;
+  t.ncols_alloc = 32;
+  while (t.ncols_alloc < ncols) t.ncols_alloc *= 2;
+  int kofs = 0, seg = 0;
+  for (int step = 0; step <= p->J; ++step) {
+    const int ti = p->J - step;
+    TcsTerm& tm = t.term[step];
+    tm.band = ti; tm.lg = ti < p->J ? ti + 1 : p->J;
+    tm.kmin = p->kmin[ti]; tm.ntap = p->cnt[ti]; tm.toff = p->toff[ti];
+    tm.ksteps = (int)cdiv(tm.ntap + 63, 16);
+    tm.kofs = kofs; kofs += tm.ksteps;
+    const int g = 1 << tm.lg;
+    tm.pos_lo = g * tm.kmin;
+    const int64_t pos_hi = p->N + (int64_t)g * (tm.kmin + 16 * tm.ksteps - 64);   // one past the last position read
+    const int64_t a = tm.pos_lo + p->ML;
+    if (a < 0) return;
+    tm.a4 = (int)(a & ~3LL);
+    const int64_t end = std::min<int64_t>(pos_hi + p->ML, p->stride);
+    tm.seg_len = (int)rup(end - tm.a4, 4);
+    tm.pad = (g >= 4 && g <= 32) ? g : 4;
+    const int64_t span = rup(pos_hi + p->ML - tm.a4, 4);        // segment indices the builders touch
+    seg = std::max<int>(seg, (int)(span + tm.pad * cdiv(span, (int64_t)64 * g)));
+  }
+  t.seg_alloc = seg;
+  p->tcs_total_ksteps = kofs;
+  t.stages = 4;
+  if (const char* e = std::getenv("SIDWT_TCS_STAGES")) t.stages = std::max(2, std::min(6, atoi(e)));
+  while (t.stages > 2 && tcs_smem_layout(t).total > 227 * 1024) --t.stages;
+  if (tcs_smem_layout(t).total > 227 * 1024) return;
+  p->tcs_smem = tcs_smem_layout(t).total;
+  p->tcs = true;
+}
+
 // Fused path: single template, taps in the kernel parameters, and a
 // tile whose on-chip bands + term results fit two CTAs per SM.
 constexpr int kFusNT = 256;
@@ -400,6 +456,7 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   if (p->d_taps) { cudaFree(p->d_taps); p->d_taps = nullptr; }
   if (p->d_partials) { cudaFree(p->d_partials); p->d_partials = nullptr; p->partials_bytes = 0; }
   if (p->d_img) { cudaFree(p->d_img); p->d_img = nullptr; }
+  if (p->d_tcs_img) { cudaFree(p->d_tcs_img); p->d_tcs_img = nullptr; }
   p->loaded = false;
   p->T = (int)T; p->n_t = n_templates;
   configure(p);
@@ -449,6 +506,23 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   }
   configure_fused(p);
   configure_tc(p);
+  configure_tcs(p);
+  if (p->tcs) {
+    const size_t img_bytes = (size_t)p->tcs_total_ksteps * kTcsAStage;
+    e = cudaMalloc(&p->d_tcs_img, img_bytes);
+    if (e == cudaSuccess) {
+      const long long items = (long long)p->tcs_total_ksteps * 4 * 128;
+      k_tcs_images<<<(unsigned)cdiv(items, 256), 256>>>(static_cast<const float2*>(p->d_taps), p->tcsp,
+                                                         p->tcs_total_ksteps, static_cast<unsigned char*>(p->d_tcs_img));
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      if (p->d_tcs_img) { cudaFree(p->d_tcs_img); p->d_tcs_img = nullptr; }
+      cudaFree(p->d_taps); p->d_taps = nullptr;
+      return cuda_status(e);
+    }
+  }
   if (p->tc) {
     const size_t img_bytes = (size_t)p->tcp.n_mt * p->tcp.total_ksteps * 8192;
     e = cudaMalloc(&p->d_img, img_bytes);
@@ -579,9 +653,31 @@ static sidwt_status correlate_tc(sidwt_plan_s* p, const void* d_bands, int64_t r
   return cuda_status(e);
 }
 
+static sidwt_status correlate_tcs(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
+                                  int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
+  TcsParams t = p->tcsp;
+  t.rows = rows;
+  if (const char* ev = std::getenv("SIDWT_TC_PROF")) t.prof = atoi(ev);
+  t.want_corr = d_corr != nullptr;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(rows, sms);
+  cudaError_t e = cudaFuncSetAttribute(k_correlate_tcs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tcs_smem);
+  if (e == cudaSuccess) {
+    k_correlate_tcs<<<(unsigned)grid, kTcsThreads, p->tcs_smem, s>>>(
+        static_cast<const float*>(d_bands), static_cast<const unsigned char*>(p->d_tcs_img), static_cast<float2*>(d_corr),
+        peaks ? d_lag : nullptr, peaks ? static_cast<float2*>(d_val) : nullptr, t);
+    e = cudaGetLastError();
+  }
+  p->last_launches = 1;
+  return cuda_status(e);
+}
+
 static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
                                    int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
   if (p->tc) return correlate_tc(p, d_bands, rows, d_corr, d_lag, d_val, peaks, s);
+  if (p->tcs) return correlate_tcs(p, d_bands, rows, d_corr, d_lag, d_val, peaks, s);
   CorParams c = p->cor;
   c.rows = rows;
   c.want_corr = d_corr != nullptr;

@@ -21,9 +21,12 @@ def _fused(plan, rows, want_corr=True):
 
 
 @pytest.mark.parametrize("cid,nrows", [(1, 1), (2, 6), (3, 2), (5, 4)])
-def test_fused_equals_two_call_path(cid, nrows):
+def test_fused_equals_two_call_path(cid, nrows, monkeypatch):
+    """Bit-identical to the two-call path through the SIMT correlation (whose item code the
+    fused kernel shares; SIDWT_TCS=0 keeps C3 off the tensor-core kernel for the comparison)."""
     from paper_cs_0607001_b200 import Plan, _native
     _native.build()
+    monkeypatch.setenv("SIDWT_TCS", "0")
     cfg = W.CONFIGS[cid]
     tm = W.templates(cfg)
     rows = W.make_rows(cfg, 0, nrows, tm)
@@ -52,9 +55,10 @@ FUSED_EDGE = [
 
 
 @pytest.mark.parametrize("fam,J,ext,N,T", FUSED_EDGE)
-def test_fused_edge(fam, J, ext, N, T):
+def test_fused_edge(fam, J, ext, N, T, monkeypatch):
     from paper_cs_0607001_b200 import Plan, _native
     _native.build()
+    monkeypatch.setenv("SIDWT_TCS", "0")
     rng = np.random.default_rng(9000 + fam * 7 + J + N)
     isint = fam == O.LEGALL53_INT
     if isint:
