@@ -150,7 +150,7 @@ sidwt_status sidwt_analyze(sidwt_plan plan, const void* d_rows, int64_t rows, vo
  * error ~1e-5 of the peak |corr| (the fp32 SIMT kernel: ~1e-7).  Environment
  * SIDWT_TC=0 disables this path, SIDWT_TC=1 forces it for any bank size; read at
  * template_load.  A single complex template with a long finest term (>= 128 taps; float
- * family, symmetric extension, N/64 in [16, 256] with the tiles fitting in shared memory,
+ * family, symmetric extension, N/64 in [16, 128] with the tiles fitting in shared memory,
  * 2^levels <= N/64) runs on the tensor
  * cores as a Toeplitz-block GEMM (the template's Toeplitz matrix against the band
  * gathered per residue class; same split precision); SIDWT_TCS=0 disables it, SIDWT_TCS=1

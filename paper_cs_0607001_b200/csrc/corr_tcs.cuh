@@ -49,6 +49,7 @@ struct TcsTerm {
 struct TcsParams {
   int N, J, stride, ML, ncols, ncols_alloc, stages, seg_alloc;
   int want_corr;
+  int merged;                                   // 1: hi | lo B products merged into one N = 2 ncols MMA
   int prof;                                     // debug (-DSIDWT_TC_PROFILE, SIDWT_TC_PROF=1): CTA 0 prints role waits
   long long rows;
   TcsTerm term[17];                             // indexed by processing step (0 = coarsest, A_J)
@@ -95,6 +96,75 @@ __global__ void k_tcs_images(const float2* __restrict__ taps, TcsParams p, int t
     split_bf16(v, hi, lo);
     const __nv_bfloat16 o = __float2bfloat16_rn(split == 0 ? hi : lo);
     *reinterpret_cast<__nv_bfloat16*>(blk + (m >> 3) * 256 + (kk >> 3) * 128 + (m & 7) * 16 + (kk & 7) * 2) = o;
+  }
+}
+
+// Builders: the B operand of every K step of one term (K-major bf16 hi / lo blocks).  Thread
+// chunk (n, h, plane) = taps j = 16 ks + 8 h + e (e < 8) of column n = blk g + r: position
+// r + g (64 blk + kmin + j), segment index off0 + r + g (64 blk + j), shared-memory index
+// idx + pad (idx >> (lg + 6)).  The chunk geometry is fixed for the term; LG >= 0 makes the
+// stride a compile-time constant.
+template <int LG>
+__device__ __forceinline__ void tcs_build_term(const TcsParams& p, const TcsTerm& tm, int tb, const float* band,
+                                               unsigned char* bst, uint64_t* bfull, uint64_t* bempty, uint32_t& qb,
+                                               long long& w_be, long long& t_build) {
+  constexpr int U = 2;                                        // chunks per thread per K step
+  const int lg = LG >= 0 ? LG : tm.lg;
+  const int g = 1 << lg, sh = lg + 6;
+  const int off0 = tm.pos_lo + p.ML - tm.a4;                  // segment index of position pos_lo
+  const int lim = p.stride - tm.a4;                           // segment indices >= lim are past the band
+  const int bstage = p.ncols * 128, bblock = p.ncols * 32;
+  int base[U], oo[U];
+  const float* src[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int ci = tb + u * 32 * kTcsBuildWarps;
+    const int n = ci % p.ncols;
+    const int h = (ci / p.ncols) & 1;
+    const int pl = ci / (2 * p.ncols);
+    const int r = n & (g - 1), blk = n >> lg;
+    base[u] = off0 + r + g * (64 * blk + 8 * h);
+    oo[u] = ci < p.ncols * 4 ? pl * 2 * bblock + (n >> 3) * 256 + h * 128 + (n & 7) * 16 : -1;
+    src[u] = band + pl * p.seg_alloc;
+  }
+  for (int ks = 0; ks < tm.ksteps; ++ks, ++qb) {
+    const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
+    TC_TWAIT(&bempty[bs], bph ^ 1, w_be);
+    const long long t_b0 = TC_CLOCK();
+    unsigned char* b0 = bst + (size_t)bs * bstage;
+    float v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i0 = base[u] + 16 * g * ks;
+      if (oo[u] < 0) {                                        // no chunk for this slot (ncols < 128)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[u][e] = 0.f;
+      } else if (i0 + 7 * g < lim) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int idx = i0 + g * e;
+          v[u][e] = src[u][idx + tm.pad * (idx >> sh)];
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int idx = i0 + g * e;
+          v[u][e] = idx < lim ? src[u][idx + tm.pad * (idx >> sh)] : 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (oo[u] < 0) continue;
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) split_bf16x2(v[u][2 * e], v[u][2 * e + 1], hi[e], lo[e]);
+      *reinterpret_cast<uint4*>(b0 + oo[u]) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(b0 + oo[u] + bblock) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(&bfull[bs]);
+    t_build += TC_CLOCK() - t_b0;
   }
 }
 
@@ -188,6 +258,8 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
           tc_fence_after();
           const uint32_t dt = tmem + db * p.ncols_alloc;
           const uint32_t idesc = idesc0;
+          const bool merged = p.merged != 0;
+          const uint32_t idesc2 = (idesc0 & ~(0x3Fu << 17)) | ((uint32_t)((2 * p.ncols) >> 3) << 17);
           for (int ks = 0; ks < tm.ksteps; ++ks, ++q, ++qb) {
             const uint32_t slot = q % S, ph = (q / S) & 1;
             const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
@@ -200,10 +272,17 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
               const uint64_t ahi = smem_desc(a0 + (pl * 2 + 0) * 4096, 128, 256);
               const uint64_t alo = smem_desc(a0 + (pl * 2 + 1) * 4096, 128, 256);
               const uint64_t bhi = smem_desc(b0 + (pl * 2 + 0) * bblock, 128, 256);
-              const uint64_t blo = smem_desc(b0 + (pl * 2 + 1) * bblock, 128, 256);
-              umma_bf16(dt, ahi, bhi, idesc, (ks > 0 || pl > 0) ? 1u : 0u);
-              umma_bf16(dt, ahi, blo, idesc, 1u);
-              umma_bf16(dt, alo, bhi, idesc, 1u);
+              if (merged) {
+                // D[:, 0:nc] += A_hi B_hi and D[:, nc:2nc] += A_hi B_lo in one MMA over the adjacent
+                // hi | lo blocks (N = 2 nc, A_hi read once), then D[:, 0:nc] += A_lo B_hi
+                umma_bf16(dt, ahi, bhi, idesc2, (ks > 0 || pl > 0) ? 1u : 0u);
+                umma_bf16(dt, alo, bhi, idesc, 1u);
+              } else {
+                const uint64_t blo = smem_desc(b0 + (pl * 2 + 1) * bblock, 128, 256);
+                umma_bf16(dt, ahi, bhi, idesc, (ks > 0 || pl > 0) ? 1u : 0u);
+                umma_bf16(dt, ahi, blo, idesc, 1u);
+                umma_bf16(dt, alo, bhi, idesc, 1u);
+              }
             }
             umma_commit(&aempty[slot]);
             umma_commit(&bempty[bs]);
@@ -225,53 +304,14 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
         if (first && tb == 0) load_band(row, step);
         first = false;
         TC_TWAIT(bandfull, qband & 1, w_band);
-        const int g = 1 << tm.lg;
-        const int off0 = tm.pos_lo + p.ML - tm.a4;                // smem index of position pos_lo
-        const int lim = p.stride - tm.a4;                         // smem indices >= lim are past the band
-        for (int ks = 0; ks < tm.ksteps; ++ks, ++qb) {
-          const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
-          TC_TWAIT(&bempty[bs], bph ^ 1, w_be);
-          const long long t_b0 = TC_CLOCK();
-          unsigned char* b0 = bst + (size_t)bs * bstage;
-          // K-major B: thread per (n, h, plane) -> taps j = 16 ks + 8 h + e of column n = blk g + r;
-          // lanes are consecutive columns; the padded band layout keeps their reads in distinct banks
-          const int sh = tm.lg + 6;
-          constexpr int U = 2;                                    // chunks in flight per thread
-          for (int c0 = tb; c0 < p.ncols * 4; c0 += U * 32 * kTcsBuildWarps) {
-            float v[U][8];
-            int oo[U], pls[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int ci = c0 + u * 32 * kTcsBuildWarps;
-              const int n = ci % p.ncols;
-              const int h = (ci / p.ncols) & 1;
-              const int pl = ci / (2 * p.ncols);
-              const int r = n & (g - 1), blk = n >> tm.lg;
-              // position r + g (64 blk + kmin + j) -> segment index off0 + r + g (64 blk + j)
-              const int i0 = off0 + r + g * (64 * blk + 16 * ks + 8 * h);
-              const float* src = band + pl * p.seg_alloc;
-              const bool ok = ci < p.ncols * 4;
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int idx = i0 + g * e;
-                v[u][e] = (ok && idx < lim) ? src[idx + tm.pad * (idx >> sh)] : 0.f;
-              }
-              oo[u] = ok ? (n >> 3) * 256 + h * 128 + (n & 7) * 16 : -1;
-              pls[u] = pl;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              if (oo[u] < 0) continue;
-              uint32_t hi[4], lo[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) split_bf16x2(v[u][2 * e], v[u][2 * e + 1], hi[e], lo[e]);
-              *reinterpret_cast<uint4*>(b0 + (pls[u] * 2 + 0) * bblock + oo[u]) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-              *reinterpret_cast<uint4*>(b0 + (pls[u] * 2 + 1) * bblock + oo[u]) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-            }
-          }
-          fence_proxy_async_smem();
-          mbar_arrive(&bfull[bs]);
-          t_build += TC_CLOCK() - t_b0;
+        switch (tm.lg) {
+          case 1: tcs_build_term<1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
+          case 2: tcs_build_term<2>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
+          case 3: tcs_build_term<3>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
+          case 4: tcs_build_term<4>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
+          case 5: tcs_build_term<5>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
+          case 6: tcs_build_term<6>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
+          default: tcs_build_term<-1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
         }
         // every builder is done with this band segment: load the next one
         named_bar(1, 32 * kTcsBuildWarps);
@@ -309,8 +349,16 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
         for (int ch = 0; ch < nch; ++ch) {
           const int n0 = ch * 32;
           uint32_t v[32];
-          tmem_ld32_nowait(tmem + db * p.ncols_alloc + ((uint32_t)(32 * quarter) << 16) + n0, v);
+          const uint32_t ta = tmem + db * p.ncols_alloc + ((uint32_t)(32 * quarter) << 16) + n0;
+          tmem_ld32_nowait(ta, v);
           tmem_wait_ld(v);
+          if (p.merged) {                                         // add the A_hi B_lo half
+            uint32_t w[32];
+            tmem_ld32_nowait(ta + p.ncols, w);
+            tmem_wait_ld(w);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(w[i]));
+          }
           if (ch == nch - 1) { tc_fence_before(); mbar_arrive(&dempty[db]); }
           // staging: row m, 32 floats, 16-byte chunks XOR-swizzled by m % 8
 #pragma unroll

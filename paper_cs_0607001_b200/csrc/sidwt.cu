@@ -358,12 +358,15 @@ static void configure_tcs(sidwt_plan_s* p) {
   if (p->paper || is_int(p) || p->n_t != 1 || p->ext != SIDWT_EXT_SYMMETRIC || p->tc) return;
   if (p->N % 64 != 0) return;
   const int ncols = (int)(p->N / 64);
-  if (ncols < 16 || ncols > 256 || ncols % 16 != 0 || (1LL << p->J) > ncols) return;
+  if (ncols < 16 || ncols > 128 || ncols % 16 != 0 || (1LL << p->J) > ncols) return;   // builders: 2 chunks/thread
   TcsParams& t = p->tcsp;
   t = TcsParams{};
   t.N = (int)p->N; t.J = p->J; t.stride = (int)p->stride; t.ML = p->ML; t.ncols = ncols;
+  // merged hi | lo products need 2 ncols TMEM columns per accumulator (double-buffered: <= 512)
+  t.merged = ncols <= 128 ? 1 : 0;
+  if (const char* e = std::getenv("SIDWT_TCS_MERGED")) t.merged = atoi(e) != 0 && ncols <= 128;
   t.ncols_alloc = 32;
-  while (t.ncols_alloc < ncols) t.ncols_alloc *= 2;
+  while (t.ncols_alloc < (t.merged ? 2 : 1) * ncols) t.ncols_alloc *= 2;
   int kofs = 0, seg = 0;
   for (int step = 0; step <= p->J; ++step) {
     const int ti = p->J - step;
