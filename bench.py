@@ -52,6 +52,14 @@ def fp32_peak_tflops(sm_mhz):
     return N_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
 
 
+IMAD_PER_CLK_PER_SM = 64    # measured (tools/micro/fma_rate.cu, profiles/r1d_micro_fma_imad.txt): half the FFMA rate
+
+
+def int32_peak_tops(sm_mhz):
+    # 148 SMs x 64 IMAD/clk x 2 int ops (multiply + add) x clock
+    return N_SMS * IMAD_PER_CLK_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -372,6 +380,13 @@ def main():
                 "note": "bf16 tensor flops = 3 x algorithmic complex-MAC flops (hi.hi + hi.lo + lo.hi)",
                 "peak_source": f"{pk['src']} MEASURED_PEAKS.json bf16_tflops_sustained"}
         comp_key, comp_bound = "tensor", "tensor"
+    elif cfg.is_int:
+        ipk = int32_peak_tops(pk["sm_mhz"])
+        comp = {"achieved": k2_tflops, "peak": ipk, "unit": "Tops/s (int32 mul+add)", "frac": k2_tflops / ipk,
+                "flops_per_row": alg["k2_flops"],
+                "peak_source": "measured IMAD rate 64/clk/SM (tools/micro/fma_rate.cu) x 148 SM x 2 x %.0f MHz"
+                               % pk["sm_mhz"]}
+        comp_key, comp_bound = "alu", "alu"
     else:
         comp = {"achieved": k2_tflops, "peak": fp32_peak, "unit": "TFLOP/s", "frac": k2_tflops / fp32_peak,
                 "flops_per_row": alg["k2_flops"],

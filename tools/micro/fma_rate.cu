@@ -26,6 +26,18 @@ __global__ void k_ffma2(float* out, float a, float b, int iters) {
   float s = 0; for (int i = 0; i < 8; ++i) { float2 v = *reinterpret_cast<float2*>(&x[i]); s += v.x + v.y; }
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+// 32-bit integer multiply-add (IMAD, wrap-around) throughput, 8 independent chains
+__global__ void k_imad(unsigned* out, unsigned a, unsigned b, int iters) {
+  unsigned x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 7u + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = x[i] * a + b;
+  }
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 int main() {
   float* d; cudaMalloc(&d, 148 * 8 * 256 * 4);
   int iters = 20000;
@@ -39,6 +51,12 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     fl = 4.0 * 8 * iters * 148.0 * 8 * 256;
     printf("FFMA2 : %.2f ms  %.1f TFLOP/s\n", ms, fl / ms / 1e9);
+    cudaEventRecord(e0); k_imad<<<148 * 8, 256>>>(reinterpret_cast<unsigned*>(d), 1664525u, 1013904223u, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 1.0 * 8 * iters * 148.0 * 8 * 256;
+    printf("IMAD  : %.2f ms  %.1f T IMAD/s  (%.1f per clk per SM at 1965 MHz)\n", ms, ops / ms / 1e9,
+           ops / (ms * 1e-3) / 148 / 1.965e9);
   }
   return 0;
 }
