@@ -480,13 +480,20 @@ __device__ __forceinline__ void corr_chunk_f(const float* __restrict__ pr, int p
   }
 }
 
+// Integer family: conj(t) w = (tx wr + ty wi) + i (tx wi - ty wr) with three multiplies,
+// k = tx (wr + wi):  re = k + (ty - tx) wi,  im = k - (tx + ty) wr  (exact in the ring of
+// integers mod 2^32, so bit-identical to the four-multiply form); ws = wr + wi is kept
+// alongside the window, so per complex MAC: 1 IMUL + 2 IMAD on the multiply pipe (half
+// rate on sm_100) and 2 IADD on the integer ALU pipe, instead of 4 IMAD.
 template <int Q, int REM, bool LAST, bool REAL = false>
 __device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int plane, int g, const int2* __restrict__ tp,
-                                             unsigned (&wr)[Q], unsigned (&wi)[Q], unsigned (&ar)[Q], unsigned (&ai)[Q]) {
+                                             unsigned (&wr)[Q], unsigned (&wi)[Q], unsigned (&ws)[Q],
+                                             unsigned (&ar)[Q], unsigned (&ai)[Q]) {
 #pragma unroll
   for (int kk = 0; kk < REM; ++kk) {
     const int2 t = tp[kk];
-    const unsigned tx = (unsigned)t.x, ty = (unsigned)t.y, nty = 0u - ty;
+    const unsigned tx = (unsigned)t.x, ty = (unsigned)t.y;
+    const unsigned d1 = ty - tx, d2 = 0u - tx - ty;
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
       const int sl = (j + kk) % Q;
@@ -494,14 +501,16 @@ __device__ __forceinline__ void corr_chunk_i(const int* __restrict__ pr, int pla
         ar[j] += tx * wr[sl];
         ai[j] += tx * wi[sl];
       } else {
-        ar[j] += tx * wr[sl] + ty * wi[sl];          // wrap-around int32 (exact mod 2^32)
-        ai[j] += tx * wi[sl] + nty * wr[sl];
+        const unsigned k = tx * ws[sl];
+        ar[j] += k + d1 * wi[sl];                    // wrap-around int32 (exact mod 2^32)
+        ai[j] += k + d2 * wr[sl];
       }
     }
     if (!LAST || kk < REM - 1) {
       const int* q = pr + kk * g;
       wr[kk] = (unsigned)q[0];
       wi[kk] = (unsigned)q[plane];
+      if (!REAL) ws[kk] = wr[kk] + wi[kk];
     }
   }
 }
@@ -511,9 +520,10 @@ __device__ __forceinline__ void corr_chunk(const typename std::conditional<INT, 
                                            const typename std::conditional<INT, int2, float2>::type* tp,
                                            typename std::conditional<INT, unsigned, float>::type (&wr)[Q],
                                            typename std::conditional<INT, unsigned, float>::type (&wi)[Q],
+                                           typename std::conditional<INT, unsigned, float>::type (&ws)[Q],
                                            typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
                                            typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
-  if constexpr (INT) corr_chunk_i<Q, REM, true, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
+  if constexpr (INT) corr_chunk_i<Q, REM, true, REAL>(pr, plane, g, tp, wr, wi, ws, ar, ai);
   else corr_chunk_f<Q, REM, true, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
 }
 
@@ -523,13 +533,14 @@ __device__ __forceinline__ void corr_last(int rem, const typename std::condition
                                           const typename std::conditional<INT, int2, float2>::type* tp,
                                           typename std::conditional<INT, unsigned, float>::type (&wr)[Q],
                                           typename std::conditional<INT, unsigned, float>::type (&wi)[Q],
+                                          typename std::conditional<INT, unsigned, float>::type (&ws)[Q],
                                           typename std::conditional<INT, unsigned, float>::type (&ar)[Q],
                                           typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
   if constexpr (R >= Q) {
-    corr_chunk<INT, Q, Q, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
+    corr_chunk<INT, Q, Q, REAL>(pr, plane, g, tp, wr, wi, ws, ar, ai);
   } else {
-    if (rem == R) corr_chunk<INT, Q, R, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
-    else corr_last<INT, Q, R + 1, REAL>(rem, pr, plane, g, tp, wr, wi, ar, ai);
+    if (rem == R) corr_chunk<INT, Q, R, REAL>(pr, plane, g, tp, wr, wi, ws, ar, ai);
+    else corr_last<INT, Q, R + 1, REAL>(rem, pr, plane, g, tp, wr, wi, ws, ar, ai);
   }
 }
 
@@ -545,7 +556,7 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
                                           typename std::conditional<INT, unsigned, float>::type (&ai)[Q]) {
   typedef typename std::conditional<INT, unsigned, float>::type A;
   const int g = 1 << lg;
-  A wr[Q], wi[Q];
+  A wr[Q], wi[Q], ws[Q];
   // received-tree orientation: outputs r + g q read W[r + g (q + k)]; the paper's orientation
   // (template tree) reads the critically sampled received band W[g (q + k)] with the
   // template's residue-r taps
@@ -554,16 +565,17 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
   for (int m = 0; m < Q; ++m) {
     wr[m] = (A)base[m << lg];
     wi[m] = (A)base[(m << lg) + plane];
+    if constexpr (INT) ws[m] = wr[m] + wi[m];
     ar[m] = A(0);
     ai[m] = A(0);
   }
   const auto* pr = base + (Q << lg);
   const int nfull = (ntap - 1) / Q;          // full chunks; the last chunk has 1..Q taps
   for (int c = 0; c < nfull; ++c, pr += Q * g, tp += Q) {
-    if constexpr (INT) corr_chunk_i<Q, Q, false, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
+    if constexpr (INT) corr_chunk_i<Q, Q, false, REAL>(pr, plane, g, tp, wr, wi, ws, ar, ai);
     else corr_chunk_f<Q, Q, false, REAL>(pr, plane, g, tp, wr, wi, ar, ai);
   }
-  corr_last<INT, Q, 1, REAL>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ar, ai);
+  corr_last<INT, Q, 1, REAL>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ws, ar, ai);
 }
 
 // All items of one term: thread item (r, qb) computes Q outputs of residue r, then the

@@ -688,7 +688,9 @@ static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t
   const int64_t grid = rows * p->n_t * c.ntiles;
   if (grid > 0x7fffffffLL) return SIDWT_ERR_RANGE;
   cudaError_t e;
-  int minb = 3;                       // 3 CTAs x 8 warps per SM (measured best on C2)
+  // 3 CTAs x 8 warps per SM (measured best on C2); the integer kernel's 3-multiply MAC keeps a
+  // third window array and runs best at 2 CTAs/SM (C5: 17.3 vs 20.1 ms at 3)
+  int minb = (is_int(p) && !p->real_taps) ? 2 : 3;
   if (const char* ev = std::getenv("SIDWT_K2_MINB")) minb = std::max(1, std::min(4, atoi(ev)));
   void (*kern)(const void*, const void*, void*, void*, const CorParams);
   const bool ct = p->ctaps;
