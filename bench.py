@@ -143,14 +143,23 @@ def plan_counts(plan):
     return [int(c) for c in cnt]
 
 
-def traffic_from_profiles(cfg_name, kernel):
+def traffic_from_profiles(cfg_name, kernel, rows=None):
+    """DRAM bytes per launch of `kernel` from profiles/ncu_traffic.json (ncu --set full:
+    dram__bytes_read.sum + dram__bytes_write.sum).  A capture on a reduced batch is stored
+    under "<cfg>_<R>rows" and scaled to `rows` (the kernels' traffic is linear in rows)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(cfg_name, {}).get(kernel)
     except Exception:
         return None
+    if kernel in d.get(cfg_name, {}):
+        return d[cfg_name][kernel]
+    for key, kern in d.items():
+        if key.startswith(cfg_name + "_") and key.endswith("rows") and kernel in kern and rows:
+            r = int(key[len(cfg_name) + 1:-4])
+            return kern[kernel] * rows / r
+    return None
 
 
 def cpu_baseline(cfg, tm, budget_s=15.0):
@@ -405,12 +414,12 @@ def main():
         use = a2 if a2["frac"] >= h2["frac"] else h2
         roof = {"kernel": k2_kernel, "bound": comp_bound if use is a2 else "hbm", "achieved": use["achieved"],
                 "peak": use["peak"], "unit": use["unit"], "frac": use["frac"],
-                "traffic": traffic_from_profiles(cfg.name, k2_kernel),
+                "traffic": traffic_from_profiles(cfg.name, k2_kernel, R),
                 "peak_source": use["peak_source"] if use is a2 else f"{pk['src']} MEASURED_PEAKS.json hbm_gbs"}
     else:
         a1 = stages["analyze"]
         roof = {"kernel": "k_analyze", "bound": "hbm", "achieved": a1["achieved"], "peak": a1["peak"],
-                "unit": "GB/s", "frac": a1["frac"], "traffic": traffic_from_profiles(cfg.name, "k_analyze"),
+                "unit": "GB/s", "frac": a1["frac"], "traffic": traffic_from_profiles(cfg.name, "k_analyze", R),
                 "peak_source": f"{pk['src']} MEASURED_PEAKS.json hbm_gbs"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
