@@ -143,6 +143,19 @@ def plan_counts(plan):
     return [int(c) for c in cnt]
 
 
+def step_roofline(stages, ms):
+    t = {}
+    for name, st in stages.items():
+        if "bytes_per_row" in st:                               # analyze: HBM only
+            t[name] = st["ms"] * st["frac"]
+        else:
+            t[name] = st["ms"] * max(v["frac"] for k, v in st.items() if isinstance(v, dict) and "frac" in v)
+    lb = sum(t.values())
+    return {"lower_bound_ms": lb, "measured_ms": ms, "frac": lb / ms,
+            "per_stage_lower_bound_ms": t,
+            "note": "per stage max(algorithmic bytes / HBM peak, algorithmic work / compute peak)"}
+
+
 def traffic_from_profiles(cfg_name, kernel, rows=None):
     """DRAM bytes per launch of `kernel` from profiles/ncu_traffic.json (ncu --set full:
     dram__bytes_read.sum + dram__bytes_write.sum).  A capture on a reduced batch is stored
@@ -431,6 +444,9 @@ def main():
                        R * (cfg.levels + 1) * 2 * plan.band_stride * 4 / 1e9,
                        R * cfg.n_templates * (cfg.levels + 1) * cfg.N * 8 / 1e9)},
         "roofline": roof,
+        # end-to-end roofline fraction = sum over stages of the algorithmic lower
+        # bound max(t_bytes, t_compute) / the measured step
+        "roofline_step": step_roofline(stages, ms),
         "stages": stages,
         "tensor_cores": tc,
         "variants": variants,
