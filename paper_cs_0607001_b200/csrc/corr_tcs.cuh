@@ -107,7 +107,7 @@ __global__ void k_tcs_images(const float2* __restrict__ taps, TcsParams p, int t
 template <int LG>
 __device__ __forceinline__ void tcs_build_term(const TcsParams& p, const TcsTerm& tm, int tb, const float* band,
                                                unsigned char* bst, uint64_t* bfull, uint64_t* bempty, uint32_t& qb,
-                                               long long& w_be, long long& t_build) {
+                                               long long& w_be, long long& t_build, long long& t_fence) {
   constexpr int U = 2;                                        // chunks per thread per K step
   const int lg = LG >= 0 ? LG : tm.lg;
   const int g = 1 << lg, sh = lg + 6;
@@ -127,12 +127,9 @@ __device__ __forceinline__ void tcs_build_term(const TcsParams& p, const TcsTerm
     oo[u] = ci < p.ncols * 4 ? pl * 2 * bblock + (n >> 3) * 256 + h * 128 + (n & 7) * 16 : -1;
     src[u] = band + pl * p.seg_alloc;
   }
-  for (int ks = 0; ks < tm.ksteps; ++ks, ++qb) {
-    const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
-    TC_TWAIT(&bempty[bs], bph ^ 1, w_be);
-    const long long t_b0 = TC_CLOCK();
-    unsigned char* b0 = bst + (size_t)bs * bstage;
-    float v[U][8];
+  // software pipelined: the band values of K step ks + 1 are loaded right after K step ks is
+  // handed over, so their shared-memory latency overlaps the wait for the next free B stage
+  auto load = [&](int ks, float (&v)[U][8]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i0 = base[u] + 16 * g * ks;
@@ -153,6 +150,14 @@ __device__ __forceinline__ void tcs_build_term(const TcsParams& p, const TcsTerm
         }
       }
     }
+  };
+  float v[U][8];
+  load(0, v);
+  for (int ks = 0; ks < tm.ksteps; ++ks, ++qb) {
+    const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
+    TC_TWAIT(&bempty[bs], bph ^ 1, w_be);
+    const long long t_b0 = TC_CLOCK();
+    unsigned char* b0 = bst + (size_t)bs * bstage;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (oo[u] < 0) continue;
@@ -162,9 +167,13 @@ __device__ __forceinline__ void tcs_build_term(const TcsParams& p, const TcsTerm
       *reinterpret_cast<uint4*>(b0 + oo[u]) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(b0 + oo[u] + bblock) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
+    const long long t_b1 = TC_CLOCK();
     fence_proxy_async_smem();
+    const long long t_b2 = TC_CLOCK();
     mbar_arrive(&bfull[bs]);
-    t_build += TC_CLOCK() - t_b0;
+    if (ks + 1 < tm.ksteps) load(ks + 1, v);
+    t_build += t_b1 - t_b0;
+    t_fence += t_b2 - t_b1;
   }
 }
 
@@ -297,7 +306,7 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
     const int tb = threadIdx.x - 32 * kTcsFirstBuild;
     uint32_t qb = 0, qband = 0;
     bool first = true;
-    long long w_band = 0, w_be = 0, t_build = 0;
+    long long w_band = 0, w_be = 0, t_build = 0, t_fence = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
       for (int step = 0; step < nterms; ++step, ++qband) {
         const TcsTerm& tm = p.term[step];
@@ -305,13 +314,13 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
         first = false;
         TC_TWAIT(bandfull, qband & 1, w_band);
         switch (tm.lg) {
-          case 1: tcs_build_term<1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
-          case 2: tcs_build_term<2>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
-          case 3: tcs_build_term<3>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
-          case 4: tcs_build_term<4>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
-          case 5: tcs_build_term<5>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
-          case 6: tcs_build_term<6>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
-          default: tcs_build_term<-1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build); break;
+          case 1: tcs_build_term<1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
+          case 2: tcs_build_term<2>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
+          case 3: tcs_build_term<3>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
+          case 4: tcs_build_term<4>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
+          case 5: tcs_build_term<5>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
+          case 6: tcs_build_term<6>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
+          default: tcs_build_term<-1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
         }
         // every builder is done with this band segment: load the next one
         named_bar(1, 32 * kTcsBuildWarps);
@@ -323,7 +332,7 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
         }
       }
     if (p.prof && blockIdx.x == 0 && tb == 0)
-      printf("tcs cta0 builder: wait band %lld bempty %lld build %lld\n", w_band, w_be, t_build);
+      printf("tcs cta0 builder: wait band %lld bempty %lld build %lld fence %lld\n", w_band, w_be, t_build, t_fence);
   } else {
     // ---------------- epilogue (128 threads, TMEM lane quarter = warp % 4)
     const int te = threadIdx.x - 32 * kTcsFirstEpi;
