@@ -99,81 +99,84 @@ __global__ void k_tcs_images(const float2* __restrict__ taps, TcsParams p, int t
   }
 }
 
-// Builders: the B operand of every K step of one term (K-major bf16 hi / lo blocks).  Thread
-// chunk (n, h, plane) = taps j = 16 ks + 8 h + e (e < 8) of column n = blk g + r: position
+// Pipeline stages: a term's K steps are taken plane by plane (all re-plane K steps, then all
+// im-plane ones), two K steps per stage, so the band segment of one plane can be reloaded for
+// the next term while the other plane is being processed.  Stage s of a term with ksteps K
+// steps: plane s / nsp, K steps 2 (s % nsp) + {0, 1} (the last stage of a plane may hold one).
+__host__ __device__ inline int tcs_nsp(int ksteps) { return (ksteps + 1) >> 1; }
+
+// Builders: the B operand of one plane's stages (K-major bf16 hi / lo blocks).  Thread chunk
+// (n, h, kk) = taps j = 16 (2 kp + kk) + 8 h + e (e < 8) of column n = blk g + r: position
 // r + g (64 blk + kmin + j), segment index off0 + r + g (64 blk + j), shared-memory index
-// idx + pad (idx >> (lg + 6)).  The chunk geometry is fixed for the term; LG >= 0 makes the
-// stride a compile-time constant.
+// idx + pad (idx >> (lg + 6)).  LG >= 0 makes the stride a compile-time constant.  Software
+// pipelined: the band values of the next stage are loaded right after a stage is handed over.
 template <int LG>
-__device__ __forceinline__ void tcs_build_term(const TcsParams& p, const TcsTerm& tm, int tb, const float* band,
-                                               unsigned char* bst, uint64_t* bfull, uint64_t* bempty, uint32_t& qb,
-                                               long long& w_be, long long& t_build, long long& t_fence) {
-  constexpr int U = 2;                                        // chunks per thread per K step
+__device__ __forceinline__ void tcs_build_phase(const TcsParams& p, const TcsTerm& tm, int tb, const float* src,
+                                                unsigned char* bst, uint64_t* bfull, uint64_t* bempty, uint32_t& qb,
+                                                long long& w_be, long long& t_build) {
+  constexpr int U = 2;                                        // chunks per thread per stage
   const int lg = LG >= 0 ? LG : tm.lg;
   const int g = 1 << lg, sh = lg + 6;
   const int off0 = tm.pos_lo + p.ML - tm.a4;                  // segment index of position pos_lo
   const int lim = p.stride - tm.a4;                           // segment indices >= lim are past the band
   const int bstage = p.ncols * 128, bblock = p.ncols * 32;
-  int base[U], oo[U];
-  const float* src[U];
+  const int nsp = tcs_nsp(tm.ksteps);
+  int base[U], oo[U], kks[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int ci = tb + u * 32 * kTcsBuildWarps;
     const int n = ci % p.ncols;
     const int h = (ci / p.ncols) & 1;
-    const int pl = ci / (2 * p.ncols);
+    const int kk = ci / (2 * p.ncols);
     const int r = n & (g - 1), blk = n >> lg;
-    base[u] = off0 + r + g * (64 * blk + 8 * h);
-    oo[u] = ci < p.ncols * 4 ? pl * 2 * bblock + (n >> 3) * 256 + h * 128 + (n & 7) * 16 : -1;
-    src[u] = band + pl * p.seg_alloc;
+    base[u] = off0 + r + g * (64 * blk + 16 * kk + 8 * h);
+    oo[u] = ci < p.ncols * 4 ? kk * 2 * bblock + (n >> 3) * 256 + h * 128 + (n & 7) * 16 : -1;
+    kks[u] = kk;
   }
-  // software pipelined: the band values of K step ks + 1 are loaded right after K step ks is
-  // handed over, so their shared-memory latency overlaps the wait for the next free B stage
-  auto load = [&](int ks, float (&v)[U][8]) {
+  auto load = [&](int kp, float (&v)[U][8]) {
+    const int kc = min(2, tm.ksteps - 2 * kp);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int i0 = base[u] + 16 * g * ks;
-      if (oo[u] < 0) {                                        // no chunk for this slot (ncols < 128)
+      const int i0 = base[u] + 32 * g * kp;
+      if (oo[u] < 0 || kks[u] >= kc) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[u][e] = 0.f;
       } else if (i0 + 7 * g < lim) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int idx = i0 + g * e;
-          v[u][e] = src[u][idx + tm.pad * (idx >> sh)];
+          v[u][e] = src[idx + tm.pad * (idx >> sh)];
         }
       } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int idx = i0 + g * e;
-          v[u][e] = idx < lim ? src[u][idx + tm.pad * (idx >> sh)] : 0.f;
+          v[u][e] = idx < lim ? src[idx + tm.pad * (idx >> sh)] : 0.f;
         }
       }
     }
   };
   float v[U][8];
   load(0, v);
-  for (int ks = 0; ks < tm.ksteps; ++ks, ++qb) {
+  for (int kp = 0; kp < nsp; ++kp, ++qb) {
+    const int kc = min(2, tm.ksteps - 2 * kp);
     const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
     TC_TWAIT(&bempty[bs], bph ^ 1, w_be);
     const long long t_b0 = TC_CLOCK();
     unsigned char* b0 = bst + (size_t)bs * bstage;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (oo[u] < 0) continue;
+      if (oo[u] < 0 || kks[u] >= kc) continue;
       uint32_t hi[4], lo[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) split_bf16x2(v[u][2 * e], v[u][2 * e + 1], hi[e], lo[e]);
       *reinterpret_cast<uint4*>(b0 + oo[u]) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(b0 + oo[u] + bblock) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
-    const long long t_b1 = TC_CLOCK();
     fence_proxy_async_smem();
-    const long long t_b2 = TC_CLOCK();
     mbar_arrive(&bfull[bs]);
-    if (ks + 1 < tm.ksteps) load(ks + 1, v);
-    t_build += t_b1 - t_b0;
-    t_fence += t_b2 - t_b1;
+    if (kp + 1 < nsp) load(kp + 1, v);
+    t_build += TC_CLOCK() - t_b0;
   }
 }
 
@@ -190,8 +193,8 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
   uint64_t* bempty = bfull + 2;                                   // [2]
   uint64_t* dfull = bempty + 2;                                   // [2]
   uint64_t* dempty = dfull + 2;                                   // [2]
-  uint64_t* bandfull = dempty + 2;                                // [1]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bandfull + 1);
+  uint64_t* bandfull = dempty + 2;                                // [2] (one per plane)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bandfull + 2);
   PeakF* red = reinterpret_cast<PeakF*>(smem_raw + 512);          // [4] epilogue warp partials
   unsigned char* ring = smem_raw + L.ring;
   unsigned char* bst = smem_raw + L.bst;
@@ -209,7 +212,8 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
       mbar_init(&bfull[i], 32 * kTcsBuildWarps); mbar_init(&bempty[i], 1);
       mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * 4);
     }
-    mbar_init(bandfull, 1);
+    mbar_init(&bandfull[0], 1);
+    mbar_init(&bandfull[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tslot, 2 * p.ncols_alloc);
@@ -221,15 +225,14 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
   // band segment of (row, step) -> smem (two planes), one thread
   // (pieces of 64 g positions, each followed by `pad` floats, so that the builders' strided
   //  reads of different 64-lag blocks fall into different banks)
-  auto load_band = [&](long long row, int step) {
+  auto load_band = [&](long long row, int step, int pl) {
     const TcsTerm& tm = p.term[step];
-    const float* src = bands + ((size_t)row * (p.J + 1) + tm.band) * 2 * p.stride + tm.a4;
+    const float* src = bands + ((size_t)row * (p.J + 1) + tm.band) * 2 * p.stride + tm.a4 + (size_t)pl * p.stride;
     const int P = 64 << tm.lg;
-    mbar_expect_tx(bandfull, 2u * tm.seg_len * 4u);
-    for (int pl = 0; pl < 2; ++pl)
-      for (int i = 0, o = 0; o < tm.seg_len; ++i, o += P)
-        bulk_load_g2s(band + pl * p.seg_alloc + i * (P + tm.pad), src + pl * p.stride + o,
-                      (uint32_t)min(P, tm.seg_len - o) * 4u, bandfull);
+    mbar_expect_tx(&bandfull[pl], tm.seg_len * 4u);
+    for (int i = 0, o = 0; o < tm.seg_len; ++i, o += P)
+      bulk_load_g2s(band + pl * p.seg_alloc + i * (P + tm.pad), src + o, (uint32_t)min(P, tm.seg_len - o) * 4u,
+                    &bandfull[pl]);
   };
 
   if (warp == 0) {
@@ -240,12 +243,16 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
       for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
         for (int step = 0; step < nterms; ++step) {
           const TcsTerm& tm = p.term[step];
-          for (int ks = 0; ks < tm.ksteps; ++ks, ++q) {
+          const int nsp = tcs_nsp(tm.ksteps);
+          for (int st = 0; st < 2 * nsp; ++st, ++q) {
+            const int pl = st / nsp, k0 = 2 * (st % nsp), kc = min(2, tm.ksteps - k0);
             const uint32_t slot = q % S, ph = (q / S) & 1;
             TC_TWAIT(&aempty[slot], ph ^ 1, w_a);
-            mbar_expect_tx(&afull[slot], kTcsAStage);
-            bulk_load_g2s(ring + (size_t)slot * kTcsAStage, img + (size_t)(tm.kofs + ks) * kTcsAStage, kTcsAStage,
-                          &afull[slot]);
+            mbar_expect_tx(&afull[slot], kc * (kTcsAStage / 2));
+            for (int kk = 0; kk < kc; ++kk)
+              bulk_load_g2s(ring + (size_t)slot * kTcsAStage + kk * (kTcsAStage / 2),
+                            img + (size_t)(tm.kofs + k0 + kk) * kTcsAStage + pl * (kTcsAStage / 2), kTcsAStage / 2,
+                            &afull[slot]);
           }
         }
       if (p.prof && blockIdx.x == 0) printf("tcs cta0 producer: wait aempty %lld\n", w_a);
@@ -269,26 +276,28 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
           const uint32_t idesc = idesc0;
           const bool merged = p.merged != 0;
           const uint32_t idesc2 = (idesc0 & ~(0x3Fu << 17)) | ((uint32_t)((2 * p.ncols) >> 3) << 17);
-          for (int ks = 0; ks < tm.ksteps; ++ks, ++q, ++qb) {
+          const int nsp = tcs_nsp(tm.ksteps);
+          for (int st = 0; st < 2 * nsp; ++st, ++q, ++qb) {
+            const int kc = min(2, tm.ksteps - 2 * (st % nsp));
             const uint32_t slot = q % S, ph = (q / S) & 1;
             const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
             TC_TWAIT(&afull[slot], ph, w_af);
             TC_TWAIT(&bfull[bs], bph, w_bf);
             tc_fence_after();
             const uint32_t a0 = ring0 + slot * kTcsAStage, b0 = bst0 + bs * bstage;
-#pragma unroll
-            for (int pl = 0; pl < 2; ++pl) {
-              const uint64_t ahi = smem_desc(a0 + (pl * 2 + 0) * 4096, 128, 256);
-              const uint64_t alo = smem_desc(a0 + (pl * 2 + 1) * 4096, 128, 256);
-              const uint64_t bhi = smem_desc(b0 + (pl * 2 + 0) * bblock, 128, 256);
+            for (int kk = 0; kk < kc; ++kk) {
+              const uint64_t ahi = smem_desc(a0 + kk * 8192, 128, 256);
+              const uint64_t alo = smem_desc(a0 + kk * 8192 + 4096, 128, 256);
+              const uint64_t bhi = smem_desc(b0 + kk * 2 * bblock, 128, 256);
+              const uint32_t acc0 = (st > 0 || kk > 0) ? 1u : 0u;
               if (merged) {
                 // D[:, 0:nc] += A_hi B_hi and D[:, nc:2nc] += A_hi B_lo in one MMA over the adjacent
                 // hi | lo blocks (N = 2 nc, A_hi read once), then D[:, 0:nc] += A_lo B_hi
-                umma_bf16(dt, ahi, bhi, idesc2, (ks > 0 || pl > 0) ? 1u : 0u);
+                umma_bf16(dt, ahi, bhi, idesc2, acc0);
                 umma_bf16(dt, alo, bhi, idesc, 1u);
               } else {
-                const uint64_t blo = smem_desc(b0 + (pl * 2 + 1) * bblock, 128, 256);
-                umma_bf16(dt, ahi, bhi, idesc, (ks > 0 || pl > 0) ? 1u : 0u);
+                const uint64_t blo = smem_desc(b0 + kk * 2 * bblock + bblock, 128, 256);
+                umma_bf16(dt, ahi, bhi, idesc, acc0);
                 umma_bf16(dt, ahi, blo, idesc, 1u);
                 umma_bf16(dt, alo, bhi, idesc, 1u);
               }
@@ -306,33 +315,37 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
     const int tb = threadIdx.x - 32 * kTcsFirstBuild;
     uint32_t qb = 0, qband = 0;
     bool first = true;
-    long long w_band = 0, w_be = 0, t_build = 0, t_fence = 0;
+    long long w_band = 0, w_be = 0, t_build = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
       for (int step = 0; step < nterms; ++step, ++qband) {
         const TcsTerm& tm = p.term[step];
-        if (first && tb == 0) load_band(row, step);
+        if (first && tb == 0) { load_band(row, step, 0); load_band(row, step, 1); }
         first = false;
-        TC_TWAIT(bandfull, qband & 1, w_band);
-        switch (tm.lg) {
-          case 1: tcs_build_term<1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
-          case 2: tcs_build_term<2>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
-          case 3: tcs_build_term<3>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
-          case 4: tcs_build_term<4>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
-          case 5: tcs_build_term<5>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
-          case 6: tcs_build_term<6>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
-          default: tcs_build_term<-1>(p, tm, tb, band, bst, bfull, bempty, qb, w_be, t_build, t_fence); break;
-        }
-        // every builder is done with this band segment: load the next one
-        named_bar(1, 32 * kTcsBuildWarps);
-        if (tb == 0) {
-          long long nrow = row;
-          int nstep = step + 1;
-          if (nstep == nterms) { nstep = 0; nrow += gridDim.x; }
-          if (nrow < p.rows) load_band(nrow, nstep);
+        for (int pl = 0; pl < 2; ++pl) {
+          TC_TWAIT(&bandfull[pl], qband & 1, w_band);
+          const float* src = band + pl * p.seg_alloc;
+          switch (tm.lg) {
+            case 1: tcs_build_phase<1>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
+            case 2: tcs_build_phase<2>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
+            case 3: tcs_build_phase<3>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
+            case 4: tcs_build_phase<4>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
+            case 5: tcs_build_phase<5>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
+            case 6: tcs_build_phase<6>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
+            default: tcs_build_phase<-1>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
+          }
+          // every builder is done with this plane's segment: load the next term's (overlaps the
+          // other plane's stages)
+          named_bar(1, 32 * kTcsBuildWarps);
+          if (tb == 0) {
+            long long nrow = row;
+            int nstep = step + 1;
+            if (nstep == nterms) { nstep = 0; nrow += gridDim.x; }
+            if (nrow < p.rows) load_band(nrow, nstep, pl);
+          }
         }
       }
     if (p.prof && blockIdx.x == 0 && tb == 0)
-      printf("tcs cta0 builder: wait band %lld bempty %lld build %lld fence %lld\n", w_band, w_be, t_build, t_fence);
+      printf("tcs cta0 builder: wait band %lld bempty %lld build %lld\n", w_band, w_be, t_build);
   } else {
     // ---------------- epilogue (128 threads, TMEM lane quarter = warp % 4)
     const int te = threadIdx.x - 32 * kTcsFirstEpi;
