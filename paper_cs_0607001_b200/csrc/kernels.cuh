@@ -578,6 +578,69 @@ __device__ __forceinline__ void corr_item(const typename std::conditional<INT, i
   corr_last<INT, Q, 1, REAL>(ntap - nfull * Q, pr, plane, g, tp, wr, wi, ws, ar, ai);
 }
 
+// Real-template item with packed FP32 pairs: the window holds (wr, wi) pairs and the
+// accumulator (ar, ai) pairs, and every tap is one fma.rn.f32x2 (FFMA2) per output instead
+// of two FFMAs -- each lane of the pair is the same fused multiply-add, so results are
+// bit-identical (the tap's real part is duplicated into both lanes).
+__device__ __forceinline__ unsigned long long f2pack(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long v, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
+}
+__device__ __forceinline__ void ffma2(unsigned long long& a, unsigned long long t, unsigned long long w) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(t), "l"(w));
+}
+
+template <int Q, int REM, bool LAST>
+__device__ __forceinline__ void corr_chunk_r2(const float* __restrict__ pr, int plane, int g,
+                                              const float2* __restrict__ tp,
+                                              unsigned long long (&w)[Q], unsigned long long (&a)[Q]) {
+#pragma unroll
+  for (int kk = 0; kk < REM; ++kk) {
+    const float tx = tp[kk].x;                                 // constant cache
+    const unsigned long long t = f2pack(tx, tx);
+#pragma unroll
+    for (int j = 0; j < Q; ++j) ffma2(a[j], t, w[(j + kk) % Q]);
+    if (!LAST || kk < REM - 1) {
+      const float* q = pr + kk * g;
+      w[kk] = f2pack(q[0], q[plane]);
+    }
+  }
+}
+
+template <int Q, int R>
+__device__ __forceinline__ void corr_last_r2(int rem, const float* pr, int plane, int g, const float2* tp,
+                                             unsigned long long (&w)[Q], unsigned long long (&a)[Q]) {
+  if constexpr (R >= Q) {
+    corr_chunk_r2<Q, Q, true>(pr, plane, g, tp, w, a);
+  } else {
+    if (rem == R) corr_chunk_r2<Q, R, true>(pr, plane, g, tp, w, a);
+    else corr_last_r2<Q, R + 1>(rem, pr, plane, g, tp, w, a);
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void corr_item_r2(const float* sb, int plane, const float2* tp, int ntap, int r, int lg,
+                                             int q0, float (&ar)[Q], float (&ai)[Q]) {
+  const int g = 1 << lg;
+  unsigned long long w[Q], a[Q];
+  const float* base = sb + r + (q0 << lg);
+#pragma unroll
+  for (int m = 0; m < Q; ++m) {
+    w[m] = f2pack(base[m << lg], base[(m << lg) + plane]);
+    a[m] = 0ull;
+  }
+  const float* pr = base + (Q << lg);
+  const int nfull = (ntap - 1) / Q;
+  for (int c = 0; c < nfull; ++c, pr += Q * g, tp += Q) corr_chunk_r2<Q, Q, false>(pr, plane, g, tp, w, a);
+  corr_last_r2<Q, 1>(ntap - nfull * Q, pr, plane, g, tp, w, a);
+#pragma unroll
+  for (int m = 0; m < Q; ++m) f2unpack(a[m], ar[m], ai[m]);
+}
+
 // All items of one term: thread item (r, qb) computes Q outputs of residue r, then the
 // eq. (4) suffix sum corr_ti = corr_{ti+1} + term into the other accumulator buffer.
 // LG >= 0: g = 2^LG is a compile-time constant; LG = -1: runtime lg.
@@ -597,7 +660,8 @@ __device__ __forceinline__ void corr_term(const typename std::conditional<INT, i
     const int r = w & (g - 1);
     const int q0 = (w >> lg) * Q;
     A ar[Q], ai[Q];
-    corr_item<INT, Q, PAPER, REAL>(sb, plane, tp + (PAPER ? r * tm.npad : 0), tm.ntap, r, lg, q0, ar, ai);
+    if constexpr (!INT && REAL && !PAPER) corr_item_r2<Q>(sb, plane, tp, tm.ntap, r, lg, q0, ar, ai);
+    else corr_item<INT, Q, PAPER, REAL>(sb, plane, tp + (PAPER ? r * tm.npad : 0), tm.ntap, r, lg, q0, ar, ai);
     // eq. (4) suffix sum: corr_ti = corr_{ti+1} + term (outputs r + g (q0 + j))
     const int base = r + (q0 << lg);
     const T2* pp = aprev + base;

@@ -525,6 +525,7 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   configure_fused(p);
   configure_tc(p);
   configure_tcs(p);
+
   if (p->tcs) {
     const size_t img_bytes = (size_t)p->tcs_total_ksteps * kTcsAStage;
     e = cudaMalloc(&p->d_tcs_img, img_bytes);
