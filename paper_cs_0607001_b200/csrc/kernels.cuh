@@ -821,8 +821,14 @@ __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__
         if (dst) *reinterpret_cast<T4*>(dst + tl) = v;
         if (p.want_peaks) {
           if constexpr (INT) {
-            consider(v.x, v.y, tau0 + tl);
-            consider(v.z, v.w, tau0 + tl + 1);
+            // pair maximum first (ties keep the earlier lag), then one compare with the best
+            const unsigned long long m0 = mag2i(v.x, v.y), m1 = mag2i(v.z, v.w);
+            const bool k0 = m0 >= m1;
+            const unsigned long long mx = k0 ? m0 : m1;
+            if (best.tau < 0 || mx > best.m2) {
+              best.m2 = mx; best.tau = tau0 + tl + (k0 ? 0 : 1);
+              best.re = k0 ? v.x : v.z; best.im = k0 ? v.y : v.w;
+            }
           } else {
             const float m0 = mag2f(v.x, v.y), m1 = mag2f(v.z, v.w);
             const float mx = fmaxf(m0, m1);
@@ -843,16 +849,16 @@ __global__ void __launch_bounds__(NT, MINB) k_correlate(const void* __restrict__
     }
     if (p.want_peaks) {
       if constexpr (INT) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          PK o;
-          o.m2 = __shfl_down_sync(0xffffffffu, best.m2, off);
-          o.tau = __shfl_down_sync(0xffffffffu, best.tau, off);
-          o.re = __shfl_down_sync(0xffffffffu, best.re, off);
-          o.im = __shfl_down_sync(0xffffffffu, best.im, off);
-          if (o.tau >= 0 && (best.tau < 0 || beats(o.m2, o.tau, best.m2, best.tau))) best = o;
-        }
-        if ((threadIdx.x & 31) == 0) red[ti][threadIdx.x >> 5] = best;
+        // warp argmax of the 64-bit |.|^2 by three hardware reductions: the largest high word,
+        // the largest low word among those lanes, then the smallest lag attaining both
+        const bool ok = best.tau >= 0;
+        const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
+        const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
+        const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
+        if (ok && (unsigned)best.tau == tmin) red[ti][threadIdx.x >> 5] = best;
+        else if ((threadIdx.x & 31) == 0 && tmin == 0xffffffffu) { PK e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; red[ti][threadIdx.x >> 5] = e; }
       } else {
         // warp argmax by two hardware reductions: the largest |.|^2 (float bits of a
         // non-negative float order like unsigned ints), then the smallest lag attaining it
