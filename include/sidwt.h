@@ -26,8 +26,10 @@
  *
  * Families (lifting programs, section III):
  *   SIDWT_LEGALL53      LeGall 5/3, PAPER.md:187-213 (dual program PAPER.md:211)
- *   SIDWT_CDF97         CDF 9/7 with Table I's rational parameters,
- *                       PAPER.md:215-244 (reading R-D3 of the garbled grids)
+ *   SIDWT_CDF97         CDF 9/7 with Table I's rational parameters (t = 5/4),
+ *                       PAPER.md:215-244 (reading R-D3 of the garbled grids); any t
+ *                       of the paper's family, incl. the irrational CDF 9/7, via
+ *                       sidwt_plan_set_lifting_t
  *   SIDWT_DAUB4_CAUSAL  causal Daubechies-4, eq. (17)
  *                       (readings R-D1: pairs (x[2k], x[2k-1]); R-D2)
  *   SIDWT_LEGALL53_INT  reversible integer 5/3 (floor-rounded predict/update,
@@ -38,7 +40,8 @@
  *   - Device pointers are caller-owned (e.g. torch tensors' data_ptr()), 16-byte
  *     aligned.  Host pointers are caller-owned.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every device
- *     call is stream-ordered and non-blocking; no call synchronises the host.
+ *     call is stream-ordered and non-blocking; only the setup call
+ *     sidwt_template_load synchronises the host (it builds the template tables).
  *     Launch failures return SIDWT_ERR_CUDA; faults inside kernels surface at
  *     the caller's next synchronisation.  No C++ exception crosses the ABI.
  *   - A plan is used by one stream at a time; it holds no global state.
