@@ -4,10 +4,14 @@
 One step = one pass of the whole hot path over one batch:
 sidwt_analyze (fused J-level lifting, all shift branches) + sidwt_correlate_peaks
 (correlation at every scale and lag, written to HBM, plus the per-scale peak
-search), on inputs already resident in HBM.  Workload: BASELINE.json configs[1]
-(C2, causal Daubechies-4, J=5, symmetric, 4096 x 4096 complex64, Barker-13x10),
-override with --config.  Multi-GPU (torchrun): weak scaling, each rank its own
-batch of rows, no collective on the data path.
+search), on inputs already resident in HBM.  Workload: BASELINE.json configs[4]
+(C5: reversible integer 5/3, J=8, symmetric, 65536 x 4096 int16 I/Q rows, 12-bit
+LFM template) -- the largest single-GPU configuration by samples per step, the
+metric naming no config; override with --config.  The line carries `parity`: the
+GPU outputs of the rows the cpu_baseline oracle processed (>= 256 seeded rows;
+C4: 16 pulses x 64 templates) compared with the oracle's.  Multi-GPU (torchrun):
+weak scaling, each rank its own batch of rows, no collective on the data path
+(DESIGN.md section 8).
 
 --impl reference times the CPU oracle (oracle/, fp64 C, OpenMP) on the host
 cores, each step a bounded row sample of the same workload.
@@ -175,19 +179,41 @@ def traffic_from_profiles(cfg_name, kernel, rows=None):
     return None
 
 
-def cpu_baseline(cfg, tm, budget_s=15.0):
-    """The oracle as it stands, on the host cores, on a bounded row sample."""
+def parity_rows(cfg, n, total):
+    """Seeded spread sample of n of the `total` row ids (always the first and the last row)."""
+    if n >= total:
+        return list(range(total))
+    rng = np.random.default_rng(np.random.SeedSequence([W.SEED_TAG, cfg.cid, 0xB]))
+    ids = set(rng.choice(np.arange(1, total - 1), size=n - 2, replace=False).tolist())
+    return sorted(ids | {0, total - 1})
+
+
+def oracle_sample(cfg, tm, rows_total, budget_s=15.0, min_rows=None):
+    """The row sample the oracle runs on: >= 256 seeded rows (C4: 16 pulses x all 64
+    templates), grown to ~budget_s of CPU work on the host cores.
+    Returns (rows, ids, threads); run_oracle_sample times the oracle on them and the same
+    rows are compared with the GPU's outputs."""
     import oracle as O
     threads = O.max_threads()
-    probe = W.make_rows(cfg, 0, min(cfg.rows, threads), tm)
+    if min_rows is None:
+        min_rows = 16 if cfg.n_templates > 1 else 256
+    min_rows = min(min_rows, rows_total)
+    probe_ids = parity_rows(cfg, min(rows_total, max(2, threads)), rows_total)
+    probe = np.stack([W.make_rows(cfg, r, 1, tm)[0] for r in probe_ids])
     t0 = time.perf_counter()
     O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, probe, tm, corr=True, nthreads=threads)
-    dt = max(time.perf_counter() - t0, 1e-6)
-    per_row = dt / probe.shape[0]
-    n = int(max(probe.shape[0], min(cfg.rows, budget_s / per_row)))
-    rows = W.make_rows(cfg, 0, n, tm)
+    per_row = max(time.perf_counter() - t0, 1e-6) / probe.shape[0]
+    n = int(max(min_rows, min(rows_total, budget_s / per_row)))
+    ids = parity_rows(cfg, n, rows_total)
+    rows = np.stack([W.make_rows(cfg, r, 1, tm)[0] for r in ids])
+    return rows, ids, threads
+
+
+def run_oracle_sample(cfg, tm, rows, ids, threads, ML, stride):
+    import oracle as O
     t0 = time.perf_counter()
-    O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, rows, tm, corr=True, nthreads=threads)
+    ref = O.run(cfg.family, cfg.levels, cfg.ext, cfg.N, rows, tm, p_lo=-ML, p_hi=stride - ML, corr=True,
+                nthreads=threads)
     dt = time.perf_counter() - t0
     cpu = ""
     try:
@@ -197,9 +223,58 @@ def cpu_baseline(cfg, tm, budget_s=15.0):
                 break
     except Exception:
         pass
-    return {"value": n * cfg.N / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"{n} of {cfg.rows} rows of {cfg.name} (full N={cfg.N}, all {cfg.levels + 1} scales, "
-                      f"{cfg.n_templates} template(s)), fp64 C oracle, {dt:.1f} s, cpu '{cpu}'"}
+    rec = {"value": len(ids) * cfg.N / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+           "sample": f"{len(ids)} of {cfg.rows} rows of {cfg.name} (seeded spread sample incl. first and last; full "
+                     f"N={cfg.N}, bands + all {cfg.levels + 1} scales + peaks, {cfg.n_templates} template(s)), "
+                     f"fp64/int64 C oracle, {dt:.1f} s, cpu '{cpu}'"}
+    return rec, ref
+
+
+BAND_RTOL, CORR_TOL = 1e-5, 1e-4     # BASELINE.json north star (tests/parity.py uses the same)
+
+
+def parity_record(cfg, ids, ref, g):
+    """GPU outputs g (bands [n][J+1][2][stride], corr [n][n_t][J+1][N][2], lag, val) of the rows
+    `ids` against the oracle's: the north-star bars (fp32: band rel L2 <= 1e-5 per (row, band),
+    corr max|err| <= 1e-4 x peak per (row, template, scale), lags exact or counted near ties;
+    integer family: everything bit-exact)."""
+    out = {"rows": len(ids), "row_ids": f"{len(ids)} seeded ids in [0, {cfg.rows}), first {ids[:4]}, last {ids[-1]}"}
+    gb, gc, gl, gv = g["bands"], g["corr"], g["lag"], g["val"]
+    if cfg.is_int:
+        ob = ref["bands"]
+        gbb = np.stack([gb[:, :, 0, :], gb[:, :, 1, :]], axis=-1).astype(np.int64)
+        bands_ok = bool(np.array_equal(gbb, ob))
+        corr_ok = bool(np.array_equal(gc, ref["corr"]))
+        lags_exact = int((gl == ref["lag"]).sum())
+        vals_ok = bool(np.array_equal(gv, ref["val"]))
+        out.update({"bit_exact_bands": bands_ok, "bit_exact_corr": corr_ok, "bit_exact_vals": vals_ok,
+                    "lags_total": int(gl.size), "lags_exact": lags_exact, "near_ties": 0,
+                    "pass": bands_ok and corr_ok and vals_ok and lags_exact == gl.size})
+        return out
+    ob = ref["bands"]
+    gbc = gb[:, :, 0, :].astype(np.float64) + 1j * gb[:, :, 1, :]
+    num = np.sqrt((np.abs(gbc - ob) ** 2).sum(-1))
+    den = np.sqrt((np.abs(ob) ** 2).sum(-1))
+    zero = den <= 1e-9 * den[:, -1:]                 # numerically-zero bands (reading R-TOL)
+    rel = np.where(zero, num / np.maximum(den[:, -1:], 1e-300), num / np.maximum(den, 1e-300))
+    oc = ref["corr"]
+    gcc = gc[..., 0].astype(np.float64) + 1j * gc[..., 1]
+    peak = np.abs(oc).max(-1)
+    err = np.abs(gcc - oc).max(-1) / np.maximum(peak, 1e-300)
+    ol = ref["lag"]
+    same = gl == ol
+    near, bad = 0, 0
+    for i in map(tuple, np.argwhere(~same)):
+        tol = CORR_TOL * peak[i]
+        if np.abs(oc[i][gl[i]]) >= np.abs(oc[i][ol[i]]) - 2 * tol:
+            near += 1
+        else:
+            bad += 1
+    out.update({"band_rel_l2_max": float(rel.max()), "band_rtol": BAND_RTOL,
+                "corr_err_over_peak_max": float(err.max()), "corr_tol": CORR_TOL,
+                "lags_total": int(gl.size), "lags_exact": int(same.sum()), "near_ties": near, "lag_failures": bad,
+                "pass": bool(rel.max() <= BAND_RTOL and err.max() <= CORR_TOL and bad == 0)})
+    return out
 
 
 def run_reference(args, cfg, rank, world):
@@ -240,7 +315,8 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5,
+                    help="BASELINE.json config (default 5: C5, the largest single-GPU workload by samples per step)")
     ap.add_argument("--rows", type=int, default=0, help="override batch rows (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -335,22 +411,18 @@ def main():
     for k in list(variants):
         variants[k.replace("_ms", "_samples_per_s")] = world * R * cfg.N / (variants[k] * 1e-3)
 
-    # timed region: K steps, barrier + sync on both sides, max over ranks
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    # timed region: K steps, barrier + sync on both sides, CUDA events on the launching
+    # stream, max over ranks (paper_cs_0607001_b200.dist.timed_steps, also driven by the
+    # world-size-2 gloo test)
+    def cuda_timer():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        return (lambda: e0.record(stream)), (lambda: e1.record(stream)), (lambda: e0.elapsed_time(e1))
     with ClockSampler(local) as clk:
-        t0.record(stream)
-        for _ in range(args.steps):
-            step()
-        t1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = D.max_over_ranks(t0.elapsed_time(t1) / args.steps, device=dev)
+        ms = D.timed_steps(step, args.steps, torch.cuda.synchronize, cuda_timer, device=dev)
     value = world * R * cfg.N / (ms * 1e-3)
+    # optional collective of the path: the per-row peak tables of every rank,
+    # all-gathered outside the timed region
+    gathered_rows = int(D.gather_weak(lag).shape[0]) if world > 1 else R
 
     # e2e: host rows (pinned) -> device -> path -> lag/val back to host, through the C ABI
     e2e = None
@@ -451,12 +523,22 @@ def main():
         "tensor_cores": tc,
         "variants": variants,
         "gpu_launches": launches_per_step * args.steps,
+        "peaks_gathered_rows": gathered_rows,
         "clocks": clk.summary(),
     }
     if e2e:
         line["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(cfg, tm)
+        # the oracle on a bounded seeded sample of this rank's rows, timed on the host cores;
+        # the GPU outputs of the same rows (last timed step) are compared with it element by
+        # element (parity on the oracle's rows)
+        o_rows, ids, threads = oracle_sample(cfg, tm, R)
+        rec, ref = run_oracle_sample(cfg, tm, o_rows, ids, threads, plan.band_offset, plan.band_stride)
+        line["cpu_baseline"] = rec
+        it = torch.tensor(ids, dtype=torch.long, device=dev)
+        g = {"bands": bands.index_select(0, it).cpu().numpy(), "corr": corr.index_select(0, it).cpu().numpy(),
+             "lag": lag.index_select(0, it).cpu().numpy(), "val": val.index_select(0, it).cpu().numpy()}
+        line["parity"] = parity_record(cfg, ids, ref, g)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -131,6 +131,11 @@ sidwt_status sidwt_plan_destroy(sidwt_plan plan);
  * sidwt_band_stride / sidwt_band_offset.  May be called again (reload). */
 sidwt_status sidwt_template_load(sidwt_plan plan, const void* host_templates, int64_t T,
                                  int n_templates);
+/* Errors of template_load: LENGTH / DIMENSION as above; RANGE when the plan's tiles do
+ * not fit the device (the analysis lifts one shift branch per thread at the deepest
+ * level, 2^(levels-1) branches in at most 512 threads, so levels <= 10 in practice;
+ * shared-memory tiles of K1 / K2 over 200 KB).  All of these are detected before any
+ * state changes: a rejected (re)load leaves the previously loaded template usable. */
 
 /* Decompose rows by lifting (every level, both shift branches).
  * d_rows : device, [rows][N] complex64, or int16x2 for the integer family.
@@ -216,11 +221,14 @@ sidwt_status sidwt_synthesize(sidwt_plan plan, const void* d_bands, int64_t rows
 
 /* End-to-end from HOST memory: copy rows host->device, analyze, correlate,
  * peaks, copy lag (and val if non-NULL) device->host, ordered on `stream`.
- * Internally pipelined over row chunks on two plan-owned streams (the copy of
- * chunk k overlaps the computation of chunk k-1), joined to `stream` by events.
- * Uses plan-owned device buffers (allocated on first use for `batch` rows;
- * SIDWT_ERR_OOM if they do not fit).  h_rows must be pinned for the overlap.
- * Returns after enqueueing; synchronise `stream` before reading h_lag/h_val. */
+ * The correlation runs in its peaks-only mode (only lag / val are returned, so
+ * corr is never written to HBM).  Internally pipelined over row chunks on two
+ * plan-owned streams (the copy of chunk k overlaps the computation of chunk
+ * k-1), joined to `stream` by events.  Uses plan-owned device buffers for
+ * `batch` rows (rows, bands, lag, val), allocated on first use and reallocated
+ * when a template reload grows the band stride or the bank; SIDWT_ERR_OOM if
+ * they do not fit.  h_rows must be pinned for the overlap.  Returns after
+ * enqueueing; synchronise `stream` before reading h_lag/h_val. */
 sidwt_status sidwt_execute_host(sidwt_plan plan, const void* h_rows, int64_t rows,
                                 int32_t* h_lag, void* h_val, void* stream);
 

@@ -49,6 +49,7 @@ struct sidwt_plan_s {
   // K1 configuration
   AnaParams ana{};
   int ana_threads = 0;
+  int64_t ana_threads_needed = 0;  // K1 threads the deepest level needs (> 512: plan rejected, RANGE)
   size_t ana_smem = 0;
   // K2 configuration
   CorParams cor{};
@@ -56,7 +57,10 @@ struct sidwt_plan_s {
   // workspaces
   void* d_partials = nullptr;
   size_t partials_bytes = 0;
-  void *w_rows = nullptr, *w_bands = nullptr, *w_corr = nullptr, *w_lag = nullptr, *w_val = nullptr;
+  // execute_host workspaces and their allocated sizes (reallocated when a template reload
+  // grows the band stride or the bank)
+  void *w_rows = nullptr, *w_bands = nullptr, *w_lag = nullptr, *w_val = nullptr;
+  size_t w_rows_bytes = 0, w_bands_bytes = 0, w_lag_bytes = 0, w_val_bytes = 0;
   // execute_host pipeline
   cudaStream_t s_copy = nullptr, s_comp = nullptr;
   cudaEvent_t ev[10] = {};
@@ -123,9 +127,10 @@ sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t 
 }
 
 static void free_ws(sidwt_plan_s* p) {
-  void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_corr, &p->w_lag, &p->w_val, &p->d_img,
+  void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_lag, &p->w_val, &p->d_img,
                    &p->d_tcs_img};
   for (void** b : bufs) { if (*b) cudaFree(*b); *b = nullptr; }
+  p->w_rows_bytes = p->w_bands_bytes = p->w_lag_bytes = p->w_val_bytes = 0;
   for (cudaEvent_t& ev : p->ev) { if (ev) cudaEventDestroy(ev); ev = nullptr; }
   if (p->d_fpartials) { cudaFree(p->d_fpartials); p->d_fpartials = nullptr; p->fpartials_bytes = 0; }
   delete p->fus; p->fus = nullptr;
@@ -275,7 +280,8 @@ static void configure(sidwt_plan_s* p) {
   const int64_t htop = 1LL << (J - 1);
   p->ana.padl = (int)rup(HL * htop, 4);
   p->ana.padr = (int)rup((kRV - 1 + HR) * htop, 4);
-  p->ana_threads = (int)std::min<int64_t>(512, rup(threads, 32));
+  p->ana_threads_needed = rup(threads, 32);
+  p->ana_threads = (int)std::min<int64_t>(512, p->ana_threads_needed);
   p->ana_smem = (size_t)(p->ana.padl + 2 * (lbuf + p->ana.padr)) * 4;
 
   // ---- K2 tiling
@@ -471,6 +477,19 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   if (!p || !host_templates) return SIDWT_ERR_PARAM;
   if (T < 1 || T > p->N) return SIDWT_ERR_LENGTH;
   if (n_templates < 1 || n_templates > 65536) return SIDWT_ERR_DIMENSION;
+  // validate the new layout before touching the loaded state: a rejected reload leaves the
+  // previous template (and every buffer) usable
+  {
+    sidwt_plan_s* trial = new (std::nothrow) sidwt_plan_s(*p);
+    if (!trial) return SIDWT_ERR_OOM;
+    trial->T = (int)T; trial->n_t = n_templates;
+    configure(trial);
+    // K1 lifts one branch per thread at the deepest level (2^(J-1) branches): at most 512
+    // threads, i.e. J <= 10 in practice; K1/K2 shared-memory tiles must fit
+    const bool fits = trial->cor_smem <= 200 * 1024 && trial->ana_smem <= 200 * 1024 && trial->ana_threads_needed <= 512;
+    delete trial;
+    if (!fits) return SIDWT_ERR_RANGE;
+  }
   if (p->d_taps) { cudaFree(p->d_taps); p->d_taps = nullptr; }
   if (p->d_partials) { cudaFree(p->d_partials); p->d_partials = nullptr; p->partials_bytes = 0; }
   if (p->d_img) { cudaFree(p->d_img); p->d_img = nullptr; }
@@ -478,7 +497,6 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   p->loaded = false;
   p->T = (int)T; p->n_t = n_templates;
   configure(p);
-  if (p->cor_smem > 200 * 1024 || p->ana_smem > 200 * 1024) return SIDWT_ERR_RANGE;
 
   const size_t tab_bytes = (size_t)n_templates * p->taps_per_t * 8;
   const size_t x_bytes = (size_t)n_templates * T * sample_bytes(p);
@@ -872,12 +890,21 @@ sidwt_status sidwt_execute_host(sidwt_plan p, const void* h_rows, int64_t rows, 
   if (!p->loaded) return SIDWT_ERR_STATE;
   if (rows < 1 || rows > p->batch) return SIDWT_ERR_DIMENSION;
   cudaError_t e = cudaSuccess;
+  // plan-owned workspaces for `batch` rows, sized from the current layout (a template reload
+  // may grow the band stride or the bank: reallocate then)
   const size_t cnt = (size_t)p->batch * p->n_t * (p->J + 1);
-  if (!p->w_rows) e = cudaMalloc(&p->w_rows, (size_t)p->batch * p->N * sample_bytes(p));
-  if (e == cudaSuccess && !p->w_bands) e = cudaMalloc(&p->w_bands, (size_t)sidwt_bands_bytes(p, p->batch));
-  if (e == cudaSuccess && !p->w_corr) e = cudaMalloc(&p->w_corr, (size_t)sidwt_corr_bytes(p, p->batch));
-  if (e == cudaSuccess && !p->w_lag) e = cudaMalloc(&p->w_lag, cnt * 4);
-  if (e == cudaSuccess && !p->w_val) e = cudaMalloc(&p->w_val, cnt * 8);
+  auto ensure = [&](void*& buf, size_t& have, size_t need) {
+    if (e != cudaSuccess || have >= need) return;
+    if (buf) cudaFree(buf);
+    buf = nullptr;
+    have = 0;
+    e = cudaMalloc(&buf, need);
+    if (e == cudaSuccess) have = need;
+  };
+  ensure(p->w_rows, p->w_rows_bytes, (size_t)p->batch * p->N * sample_bytes(p));
+  ensure(p->w_bands, p->w_bands_bytes, (size_t)sidwt_bands_bytes(p, p->batch));
+  ensure(p->w_lag, p->w_lag_bytes, cnt * 4);
+  ensure(p->w_val, p->w_val_bytes, cnt * 8);
   if (e == cudaSuccess && !p->s_copy) e = cudaStreamCreateWithFlags(&p->s_copy, cudaStreamNonBlocking);
   if (e == cudaSuccess && !p->s_comp) e = cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking);
   for (int k = 0; e == cudaSuccess && k < kPipeChunks + 2; ++k)
@@ -906,13 +933,13 @@ sidwt_status sidwt_execute_host(sidwt_plan p, const void* h_rows, int64_t rows, 
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_comp, p->ev[k], 0);
     if (e != cudaSuccess) return cuda_status(e);
     char* dbands = static_cast<char*>(p->w_bands) + (size_t)sidwt_bands_bytes(p, r0);
-    char* dcorr = static_cast<char*>(p->w_corr) + (size_t)sidwt_corr_bytes(p, r0);
     int32_t* dlag = static_cast<int32_t*>(p->w_lag) + r0 * per_row_out;
     char* dval = static_cast<char*>(p->w_val) + (size_t)r0 * per_row_out * 8;
     st = sidwt_analyze(p, drows, nr, dbands, p->s_comp);
     if (st != SIDWT_OK) return st;
     launches += p->last_launches;
-    st = sidwt_correlate_peaks(p, dbands, nr, dcorr, dlag, dval, p->s_comp);
+    // peaks only: the call returns lag / val, so the correlation is not written to HBM
+    st = sidwt_correlate_peaks(p, dbands, nr, nullptr, dlag, dval, p->s_comp);
     if (st != SIDWT_OK) return st;
     launches += p->last_launches;
     e = cudaMemcpyAsync(h_lag + r0 * per_row_out, dlag, (size_t)nr * per_row_out * 4, cudaMemcpyDeviceToHost, p->s_comp);

@@ -47,3 +47,38 @@ def gather_rows(local, total_rows: int, device=None):
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad)
     return torch.cat([b[:n] for b, n in zip(bufs, sizes)], dim=0)
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.barrier()
+
+
+def timed_steps(step, steps: int, sync, timer, device=None) -> float:
+    """The contract's timed region, shared by bench.py (NCCL, CUDA events) and the gloo test
+    (CPU clock): barrier + sync, `steps` calls of `step`, sync + barrier, then the per-step
+    time as the MAX over ranks.  `timer()` returns a (start, stop, elapsed_ms) triple of
+    callables; `sync()` waits for the device."""
+    start, stop, elapsed_ms = timer()
+    barrier()
+    sync()
+    start()
+    for _ in range(steps):
+        step()
+    stop()
+    sync()
+    barrier()
+    return max_over_ranks(elapsed_ms() / steps, device=device)
+
+
+def gather_weak(local, device=None):
+    """All-gather equal-size per-rank row blocks of a weak-scaling run (rank order) into one
+    [world * rows, ...] tensor on every rank (e.g. the per-row peak tables)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return local
+    bufs = [torch.empty_like(local) for _ in range(dist.get_world_size())]
+    dist.all_gather(bufs, local.contiguous())
+    return torch.cat(bufs, dim=0)

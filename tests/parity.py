@@ -15,6 +15,9 @@ import oracle as O
 
 BAND_RTOL = 1e-5
 CORR_TOL = 1e-4
+NEARTIE_FRAC = 1e-3          # bound on R3 near-tie accepts per compare() call
+
+STATS = []                   # every compare() result, printed in the terminal summary (conftest.py)
 
 
 def run_gpu(plan, rows: np.ndarray, fused: bool = False):
@@ -43,6 +46,7 @@ def compare(plan, g, r, row_ids=None, check_bands=True):
     Returns stats dict."""
     J = plan.levels
     stats = dict(band_rel_l2=0.0, corr_err=0.0, lag_exact=0, lag_neartie=0)
+    STATS.append(stats)
     gb, gc, gl, gv = g["bands"], g["corr"], g["lag"], g["val"]
     if row_ids is not None:
         gb, gc, gl, gv = gb[row_ids], gc[row_ids], gl[row_ids], gv[row_ids]
@@ -54,20 +58,24 @@ def compare(plan, g, r, row_ids=None, check_bands=True):
         assert np.array_equal(gc, r["corr"]), "integer corr differs"
         assert np.array_equal(gl, r["lag"]), "integer lags differ"
         assert np.array_equal(gv, r["val"]), "integer peak values differ"
-        stats["lag_exact"] = gl.size
+        stats["lag_exact"] = int(gl.size)
+        stats["lag_total"] = int(gl.size)
         return stats
     if check_bands:
         ob = r["bands"]                                   # [rows][J+1][nb] complex
         gbc = gb[:, :, 0, :].astype(np.float64) + 1j * gb[:, :, 1, :]
         num = np.sqrt((np.abs(gbc - ob) ** 2).sum(-1))
         den = np.sqrt((np.abs(ob) ** 2).sum(-1))
-        # Degenerate bands (reading R-TOL): a band that is identically ~0 in
-        # exact arithmetic (e.g. the detail bands of a DC row, vanishing moments) has no
-        # relative error; its norm is floored at 1e-2 x the approximation band's norm.
-        floor = 1e-2 * den[:, -1:]
-        rel = num / np.maximum(np.maximum(den, floor), 1e-300)
-        rel = np.where(den + floor > 0, rel, num)
+        # Reading R-TOL: a band that is zero in exact arithmetic (the oracle's fp64 norm is
+        # <= 1e-9 x the row's U_J norm: the detail bands of a DC or zero row, vanishing
+        # moments) has no relative error of its own; its error is measured against the U_J
+        # norm instead.  Every other band: its own relative L2 error <= 1e-5.
+        ref_uj = den[:, -1:]
+        zero = den <= 1e-9 * ref_uj
+        rel = np.where(zero, num / np.maximum(ref_uj, 1e-300), num / np.maximum(den, 1e-300))
+        rel = np.where(zero & (ref_uj == 0), num, rel)     # all-zero row: the GPU must give exact zeros
         stats["band_rel_l2"] = float(rel.max())
+        stats["bands_zero"] = int(zero.sum())
         assert rel.max() <= BAND_RTOL, f"band rel L2 {rel.max():.3e} > {BAND_RTOL}"
     oc = r["corr"]
     gcc = gc[..., 0].astype(np.float64) + 1j * gc[..., 1]
@@ -88,6 +96,10 @@ def compare(plan, g, r, row_ids=None, check_bands=True):
             b = np.abs(oc[i][ol[i]])
             assert a >= b - 2 * tol, f"lag mismatch at {i}: gpu {gl[i]} oracle {ol[i]}"
             stats["lag_neartie"] += 1
+    stats["lag_total"] = int(gl.size)
+    # R3 is a safety net: exact lag agreement is expected (no top-two
+    # gap below 1e-5 in 20 000 C3-like rows), so near ties must stay rare
+    assert stats["lag_neartie"] <= max(1, int(np.ceil(NEARTIE_FRAC * gl.size))), stats
     # peak values: value of the GPU's corr at the GPU's lag
     gvc = gv[..., 0] + 1j * gv[..., 1]
     picked = np.take_along_axis(gcc, gl[..., None].astype(np.int64), -1)[..., 0]

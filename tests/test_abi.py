@@ -30,10 +30,25 @@ def test_header_symbols_exported(native):
 
 
 def test_sass_is_sm100a(native):
+    """The library is sm_100a code and each kernel family carries its Blackwell-native
+    instructions (tools/sass_evidence.py; summary in profiles/)."""
+    import collections
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import sass_evidence as SE
     out = os.popen(f"cuobjdump --list-elf {native.LIB_PATH}").read()
     assert "sm_100a" in out
-    sass = os.popen(f"cuobjdump -sass {native.LIB_PATH} 2>/dev/null").read()
-    assert "UBLKCP" in sass or "UTMASTG" in sass or "BLKCP" in sass   # TMA bulk store in k_analyze
+    per = collections.defaultdict(collections.Counter)
+    for name, lines in SE.kernels(native.LIB_PATH).items():
+        per[SE.short(name)].update(SE.counts(lines))
+    # template-bank tensor-core correlation: tcgen05.mma, tcgen05.ld, TMA tensor stores of corr
+    for k in ("UTCHMMA", "LDTM", "UTMASTG", "UBLKCP"):
+        assert per["k_correlate_tc"][k] > 0, ("k_correlate_tc", k)
+    # single-template tensor-core correlation: tcgen05.mma, tcgen05.ld, bulk copies
+    for k in ("UTCHMMA", "LDTM", "UBLKCP"):
+        assert per["k_correlate_tcs"][k] > 0, ("k_correlate_tcs", k)
+    assert per["k_analyze"]["UBLKCP"] > 0                  # TMA bulk stores of the bands
+    assert per["k_correlate"]["FFMA2"] > 0                 # packed FP32 real-template correlation
 
 
 def test_plan_validation_without_gpu(native):
@@ -68,6 +83,12 @@ def test_plan_validation_without_gpu(native):
     assert L.sidwt_template_load(plan, x, 1, 0) == 3            # DIMENSION
     assert L.sidwt_plan_destroy(plan) == 0
     assert L.sidwt_plan_destroy(None) == 0
+    # J = 11: the deepest analysis level needs 1024 branch threads > 512 -> RANGE, detected
+    # before any device work (so also without a GPU)
+    assert L.sidwt_plan_create(C.byref(h), 0, 11, 4096, 1, 0) == 0
+    assert L.sidwt_template_load(h.value, x, 1, 1) == 5
+    assert L.sidwt_band_stride(h.value) == -1
+    assert L.sidwt_plan_destroy(h.value) == 0
     assert native.sidwt_status_string(6) == "state error"
 
 

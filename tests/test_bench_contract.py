@@ -45,3 +45,44 @@ def test_traffic_scaling(tmp_path, monkeypatch):
     assert bench.traffic_from_profiles("C2", "k", 7) == 10.0                 # exact batch
     assert bench.traffic_from_profiles("C3", "k", 400) == 200.0              # scaled 100 -> 400 rows
     assert bench.traffic_from_profiles("C4", "k", 1) is None
+
+
+def _gpu_like(ref, J, is_int):
+    """The oracle's outputs cast to what the GPU returns (fp32 split planes / int32)."""
+    import numpy as np
+    b = ref["bands"]
+    if is_int:
+        bands = np.stack([b[..., 0], b[..., 1]], axis=2).astype(np.int32)
+        return {"bands": bands, "corr": ref["corr"].copy(), "lag": ref["lag"].copy(), "val": ref["val"].copy()}
+    bands = np.stack([b.real, b.imag], axis=2).astype(np.float32)
+    corr = np.stack([ref["corr"].real, ref["corr"].imag], axis=-1).astype(np.float32)
+    val = np.take_along_axis(corr, ref["lag"][..., None, None].astype(np.int64), -2)[..., 0, :]
+    return {"bands": bands, "corr": corr, "lag": ref["lag"].copy(), "val": val}
+
+
+def test_parity_record_on_the_oracle_sample():
+    """bench.py's `parity` object: the rows of the oracle sample, the tolerances of the north
+    star; a perturbed band / corr / lag fails it (float and integer families)."""
+    import numpy as np
+    import workloads as W
+    for cid in (2, 5):
+        cfg = W.CONFIGS[cid]
+        tm = W.templates(cfg)
+        rows, ids, threads = bench.oracle_sample(cfg, tm, 40, budget_s=0.0, min_rows=6)
+        assert len(ids) == 6 and ids[0] == 0 and ids[-1] == 39 and ids == sorted(set(ids))
+        assert np.array_equal(rows[1], W.make_rows(cfg, ids[1], 1, tm)[0])
+        ML, stride = 256, 4096 + 768
+        rec, ref = bench.run_oracle_sample(cfg, tm, rows, ids, 2, ML, stride)
+        assert rec["kind"] == "oracle" and rec["value"] > 0 and "6 of" in rec["sample"]
+        g = _gpu_like(ref, cfg.levels, cfg.is_int)
+        p = bench.parity_record(cfg, ids, ref, g)
+        assert p["pass"] and p["rows"] == 6 and p["lags_exact"] == p["lags_total"] == 6 * (cfg.levels + 1), p
+        bad = {k: v.copy() for k, v in g.items()}
+        bad["bands"][3, 1, 0, 300] += 1 if cfg.is_int else 1e-2
+        assert not bench.parity_record(cfg, ids, ref, bad)["pass"]
+        bad = {k: v.copy() for k, v in g.items()}
+        bad["corr"][2, 0, 0, 7, 0] += 1 if cfg.is_int else 1e3
+        assert not bench.parity_record(cfg, ids, ref, bad)["pass"]
+        bad = {k: v.copy() for k, v in g.items()}
+        bad["lag"][0, 0, 0] = (bad["lag"][0, 0, 0] + 1000) % cfg.N
+        assert not bench.parity_record(cfg, ids, ref, bad)["pass"]

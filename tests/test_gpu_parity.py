@@ -153,12 +153,20 @@ def test_execute_host_matches_device_path():
 
 # ------------------------------------------------------------------ full BASELINE sizes
 
-def _sample_rows(n, k=6):
-    return sorted(set([0, n - 1] + list(np.linspace(0, n - 1, k).astype(int))))
+def _sample_rows(cfg, n):
+    """n seeded row ids spread over the batch, always the first and the last (BASELINE.md
+    section 3: >= 256 rows for C2/C3/C5, 16 pulses for C4)."""
+    if n >= cfg.rows:
+        return list(range(cfg.rows))
+    rng = np.random.default_rng(np.random.SeedSequence([W.SEED_TAG, cfg.cid, 0xB]))
+    ids = set(rng.choice(np.arange(1, cfg.rows - 1), size=n - 2, replace=False).tolist())
+    return sorted(ids | {0, cfg.rows - 1})
 
 
 @pytest.mark.parametrize("cid", [2, 3, 5])
 def test_full_size_sampled(cid):
+    """The whole BASELINE batch through analyze + correlate_peaks (bench.py's launch
+    configuration); 256 seeded rows compared with the oracle element by element."""
     import torch
     cfg = W.CONFIGS[cid]
     tm = W.templates(cfg)
@@ -168,19 +176,23 @@ def test_full_size_sampled(cid):
     bands = plan.analyze(d_rows, cfg.rows)
     corr, lag, val = plan.correlate_peaks(bands, cfg.rows)
     torch.cuda.synchronize()
-    ids = _sample_rows(cfg.rows)
-    g = dict(bands=bands[ids].cpu().numpy(), corr=corr[ids].cpu().numpy(),
-             lag=lag[ids].cpu().numpy(), val=val[ids].cpu().numpy())
+    ids = _sample_rows(cfg, 256)
+    it = torch.tensor(ids, device=bands.device)
+    g = dict(bands=bands.index_select(0, it).cpu().numpy(), corr=corr.index_select(0, it).cpu().numpy(),
+             lag=lag.index_select(0, it).cpu().numpy(), val=val.index_select(0, it).cpu().numpy())
     r = oracle_for(plan, rows[ids], tm)
     st = compare(plan, g, r)
-    # property at any size: lags and values are self-consistent for every row
+    assert st["lag_total"] == 256 * (cfg.levels + 1)
+    # property at any size: every lag is in range
     lg = lag.cpu().numpy()
     assert lg.min() >= 0 and lg.max() < cfg.N
-    print(cfg.name, "full-size sampled", st)
+    print(cfg.name, "full-size, 256 rows vs oracle", st)
     del bands, corr
 
 
 def test_full_size_c4_sampled():
+    """C4 (2048 pulses x bank of 64) through the peaks-only bank kernel; 16 seeded pulses x all
+    64 templates compared with the oracle (corr of those pulses from the same kernel)."""
     import torch
     cfg = W.CONFIGS[4]
     tm = W.templates(cfg)
@@ -190,13 +202,18 @@ def test_full_size_c4_sampled():
     bands = plan.analyze(d_rows, cfg.rows)
     _, lag, val = plan.correlate_peaks(bands, cfg.rows, want_corr=False)     # peaks-only mode
     torch.cuda.synchronize()
-    ids = [0, cfg.rows - 1]
-    sub = plan.correlate_peaks(bands[ids].contiguous(), 2)
+    ids = _sample_rows(cfg, 16)
+    it = torch.tensor(ids, device=bands.device)
+    sub_bands = bands.index_select(0, it).contiguous()
+    sub = plan.correlate_peaks(sub_bands, len(ids))
     torch.cuda.synchronize()
-    g = dict(bands=bands[ids].cpu().numpy(), corr=sub[0].cpu().numpy(),
-             lag=lag[ids].cpu().numpy(), val=val[ids].cpu().numpy())
+    g = dict(bands=sub_bands.cpu().numpy(), corr=sub[0].cpu().numpy(),
+             lag=lag.index_select(0, it).cpu().numpy(), val=val.index_select(0, it).cpu().numpy())
+    assert np.array_equal(g["lag"], sub[1].cpu().numpy())       # peaks-only == with-corr peaks
     r = oracle_for(plan, rows[ids], tm)
-    compare(plan, g, r)
+    st = compare(plan, g, r)
+    assert st["lag_total"] == 16 * 64 * (cfg.levels + 1)
+    print(cfg.name, "full-size, 16 pulses x 64 templates vs oracle", st)
 
 
 def test_real_template_variant_equals_general_path():
@@ -217,3 +234,46 @@ def test_real_template_variant_equals_general_path():
     g2 = run_gpu(p_gen, rows, fused=True)
     assert np.array_equal(g1["corr"], g2["corr"]) and np.array_equal(g1["lag"], g2["lag"])
     compare(p_real, g1, oracle_for(p_real, rows, tm))
+
+
+def test_execute_host_after_reload_grows_workspaces():
+    """execute_host, then a reload with a longer template (wider band margins -> larger band
+    stride) and a larger bank, then execute_host again: the plan-owned workspaces must follow
+    the new layout (results equal the device path and the oracle)."""
+    import torch
+    from paper_cs_0607001_b200 import Plan, _native
+    _native.build()
+    rng = np.random.default_rng(77)
+    N, J, R = 1024, 4, 6
+    rows = (rng.normal(size=(R, N)) + 1j * rng.normal(size=(R, N))).astype(np.complex64)
+    plan = Plan(O.CDF97, J, N, R, O.SYMMETRIC)
+    for n_t, T in ((1, 16), (3, 200)):
+        tm = (rng.normal(size=(n_t, T)) + 1j * rng.normal(size=(n_t, T))).astype(np.complex64)
+        plan.load_templates(tm)
+        lag = np.zeros((R, n_t, J + 1), np.int32)
+        val = np.zeros((R, n_t, J + 1, 2), np.float32)
+        plan.execute_host(np.ascontiguousarray(rows), R, lag, val)
+        torch.cuda.synchronize()
+        g = run_gpu(plan, rows, fused=True)
+        assert np.array_equal(lag, g["lag"]) and np.array_equal(val, g["val"])
+        compare(plan, g, oracle_for(plan, rows, tm))
+
+
+def test_rejected_reload_keeps_previous_template():
+    """A reload that the layout validation rejects (RANGE) leaves the loaded template usable."""
+    import torch
+    from paper_cs_0607001_b200 import Plan, SidwtError, _native
+    _native.build()
+    rng = np.random.default_rng(5)
+    N, J, R = 8192, 10, 2
+    rows = (rng.normal(size=(R, N)) + 1j * rng.normal(size=(R, N))).astype(np.complex64)
+    tm = (rng.normal(size=(1, 40)) + 1j * rng.normal(size=(1, 40))).astype(np.complex64)
+    plan = Plan(O.LEGALL53, J, N, R, O.SYMMETRIC).load_templates(tm)
+    g0 = run_gpu(plan, rows, fused=True)
+    with pytest.raises(SidwtError) as e:
+        # T = N at J = 10: the coarsest term's band tile no longer fits the K2 shared memory
+        _native.sidwt_template_load(plan.handle, np.ones((1, N, 2), np.float32), N, 1)
+    assert e.value.status == 5
+    g1 = run_gpu(plan, rows, fused=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(g0["corr"], g1["corr"]) and np.array_equal(g0["lag"], g1["lag"])
