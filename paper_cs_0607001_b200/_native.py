@@ -13,11 +13,16 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libsidwt.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sidwt.cu", "kernels.cuh", "lifting.cuh", "corr_tc.cuh", "corr_tcs.cuh", "fused.cuh")] + [
-    os.path.join(ROOT, "include", "sidwt.h")]
+CSRC = os.path.join(HERE, "csrc")
+HEADERS = [os.path.join(CSRC, f) for f in ("kernels.cuh", "lifting.cuh", "corr_tc.cuh", "corr_tcs.cuh", "fused.cuh",
+                                           "corr_i8.h")] + [os.path.join(ROOT, "include", "sidwt.h")]
+# translation units (compiled separately, in parallel, then linked into one shared library)
+UNITS = [os.path.join(CSRC, "sidwt.cu"), os.path.join(CSRC, "corr_i8.cu")]
+SOURCES = UNITS + HEADERS
+BUILD_DIR = os.path.join(ROOT, "build")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC"]
 
 SIDWT_LEGALL53, SIDWT_CDF97, SIDWT_DAUB4_CAUSAL, SIDWT_LEGALL53_INT = 0, 1, 2, 3
 SIDWT_EXT_PERIODIC, SIDWT_EXT_SYMMETRIC = 0, 1
@@ -38,16 +43,26 @@ EXPORTS = ["sidwt_plan_create", "sidwt_plan_set_orientation", "sidwt_plan_set_li
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> paper_cs_0607001_b200/libsidwt.so"""
-    stale = not os.path.exists(LIB_PATH) or any(
-        os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in SOURCES)
-    if force or stale:
-        cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(HERE, "csrc", "sidwt.cu")]
-        if os.environ.get("SIDWT_TC_PROFILE"):        # debug: timed role waits in the tensor-core kernel
-            cmd.insert(1, "-DSIDWT_TC_PROFILE")
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd)
+    """nvcc -gencode arch=compute_100a,code=sm_100a: each translation unit of csrc/ -> build/*.o
+    (rebuilt when it or a header changed), linked into paper_cs_0607001_b200/libsidwt.so."""
+    os.makedirs(BUILD_DIR, exist_ok=True)
+    newest_hdr = max(os.path.getmtime(h) for h in HEADERS)
+    procs, objs = [], []
+    for src in UNITS:
+        obj = os.path.join(BUILD_DIR, os.path.basename(src).replace(".cu", ".o"))
+        objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), newest_hdr):
+            cmd = ["nvcc", *NVCC_FLAGS, "-c", "-o", obj, src]
+            if os.environ.get("SIDWT_TC_PROFILE"):        # debug: timed role waits in the tensor-core kernels
+                cmd.insert(1, "-DSIDWT_TC_PROFILE")
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            procs.append((subprocess.Popen(cmd), cmd))
+    for pr, cmd in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, cmd)
+    if force or procs or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(map(os.path.getmtime, objs)):
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH, *objs])
     return LIB_PATH
 
 

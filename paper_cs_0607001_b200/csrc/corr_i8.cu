@@ -1,0 +1,500 @@
+// corr_i8.cu -- integer-family correlation (a5-a7) on the tensor cores, sm_100a.
+//
+// Reversible integer 5/3 (reading R-INT): bands W_1..W_J, U_J are exact int32 and the
+// correlation is the exact integer reduced mod 2^32, so no rounding may
+// enter.  Term i (band W at stride g = 2^lg, taps t[k] at support kmin + k, k < n):
+//     D[tau] = sum_k conj(t[k]) W[tau + g (kmin + k)]               (a5)
+//
+// Exact integer GEMM by digits.  Every band value x lies in the static bound of its band
+// (interval arithmetic through the integer lifting program from int16 rows: |U_s| <= 2^s 32768,
+// |W_s| <= 2^(s-1) 65535), so x = sum_b 256^b d_b with d_b the bytes of its two's complement
+// (d_b unsigned for b < D-1, the top digit signed), D = 3 for J <= 8; D = 2 whenever a term's
+// staged values all fit in int16 (checked per row and term by the builders).  The template
+// coefficients are split into balanced signed digits t = sum_a 256^a t_a.  Each digit product
+// d_b t_a is an int8 tensor-core MMA (tcgen05.mma kind::i8) with int32 accumulation -- exact,
+// the sums stay far below 2^31 -- and the epilogue forms sum_{a,b} 256^(a+b) acc_{a,b} mod 2^32.
+//
+// GEMM shape (natural lag order, no Toeplitz matrix of the data is formed):
+//   M = 128 rows = 128 lag blocks of 16 consecutive lags (tile of 2048 lags): row c, K byte j
+//       reads the digit stream at byte 16 c + j -- a Hankel view of one byte plane of the band
+//       (K-major, no swizzle, core matrices of 8 rows x 16 bytes overlapping at a 16-byte row
+//       pitch: SBO = 128 B).
+//   N = 32 Tn columns = (output component re/im) x (template digit a) x (shift p = 0..15).
+//   K: dense terms (g < 16): consecutive 32-byte steps of the stream; B[j][p] = t_k where
+//       j - p - sh = g k.  Strided terms (g >= 16): each 16-byte K half holds one tap -- the
+//       A descriptor's leading byte offset is g, so the two halves of a K step are the
+//       16-byte windows of taps 2ks and 2ks+1 -- and B is diagonal (j mod 16 = p).
+//   conj(t) w = (tr wr + ti wi) + i (tr wi - ti wr): the wr stream meets B columns
+//   (re: tr, im: -ti), the wi stream (re: ti, im: tr); both accumulate into the same TMEM.
+//   One accumulator per data digit b: [128 lanes][ncol] int32; TMEM double-buffered by tile.
+//
+// Eq. (4): one CTA owns a whole row (persistent over rows), terms coarsest
+// first; every epilogue thread owns the same 16 lags of each 2048-lag tile for all terms, so
+// the running corr_i = corr_{i+1} + D_i lives in its registers; each corr_i goes straight to
+// HBM (128 contiguous bytes per thread) and the row's peak per scale (a7) is reduced in the
+// epilogue -- no partials, no finalize kernel.
+//
+// Roles (320 threads): warp 0 bulk-copy loader (band segments of both components, B images);
+// warp 1 MMA issuer; warps 2-5 builders (int32 band segment -> byte-digit planes, range
+// flag); warps 6-9 epilogue (TMEM lane quarter = warp % 4).
+#define SIDWT_NO_KERNELS
+#include "kernels.cuh"
+#include "corr_tc.cuh"
+#include "corr_i8.h"
+
+#include <algorithm>
+#include <vector>
+
+namespace sidwt {
+
+constexpr int kI8Warps = 10;
+constexpr int kI8Threads = 32 * kI8Warps;
+constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6;
+constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
+constexpr int kI8BufCols = 256;                     // TMEM columns per accumulator buffer (dmax * ncol <= 256)
+
+struct I8Smem { size_t band, stream, img, total; };
+__host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
+  I8Smem L;
+  L.band = 1024;                                                        // barriers, flags, peak partials below
+  L.stream = (L.band + (size_t)p.nband * 2 * p.seg_alloc * 4 + 127) & ~(size_t)127;
+  L.img = L.stream + (size_t)p.nstream * 2 * p.dmax * p.plane;
+  L.total = L.img + (size_t)p.nimg * p.img_alloc;
+  return L;
+}
+
+// D[tmem] (+)= A[smem] . B[smem], kind::i8 (int8 inputs, int32 accumulate)
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread (no wait)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :: "memory");
+}
+
+// B operand images: for each processing step, K step ks, data component x (0: wr, 1: wi), an
+// [ncol][32 bytes] K-major no-swizzle block, element (n, j) at (n/8)*256 + (j/16)*128 + (n%8)*16
+// + j%16; column n = oc (16 tn) + 16 a + p holds digit a of the coefficient that multiplies the
+// x stream for output component oc at shift p.  One thread per (step, ks, x, n).
+__global__ void k_i8_images(const int2* __restrict__ taps, I8Params p, const int* toff_by_term, int total,
+                            unsigned char* __restrict__ img) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total) return;
+  const int n = gid % p.ncol;
+  int rest = gid / p.ncol;
+  const int x = rest & 1;
+  rest >>= 1;                                         // global K-step index
+  int step = 0, base = 0;
+  while (step <= p.J && rest >= base + p.term[step].ksteps) { base += p.term[step].ksteps; ++step; }
+  const I8Term tm = p.term[step];
+  const int ks = rest - base;
+  const int ti = p.J - step;
+  const int oc = n / (16 * p.tn), a = (n / 16) % p.tn, pp = n % 16;
+  const int g = 1 << tm.lg;
+  unsigned char* blk = img + tm.img_ofs + (size_t)(ks * 2 + x) * p.ncol * 32;
+  for (int j = 0; j < 32; ++j) {
+    int k = -1;
+    if (tm.strided) {
+      if ((j & 15) == pp) k = 2 * ks + (j >> 4);
+    } else {
+      const int d = 32 * ks + j - pp - tm.sh;
+      if (d >= 0 && d % g == 0) k = d / g;
+    }
+    int dig = 0;
+    if (k >= 0 && k < tm.ntap) {
+      const int2 t = taps[toff_by_term[ti] + k];
+      // conj(t) w: wr meets (re: tr, im: -ti), wi meets (re: ti, im: tr)
+      int v = (x == 0) ? (oc == 0 ? t.x : -t.y) : (oc == 0 ? t.y : t.x);
+      for (int q = 0; q <= a; ++q) {                   // balanced base-256 digit a
+        dig = ((v + 128) & 255) - 128;
+        v = (v - dig) >> 8;
+      }
+    }
+    blk[(n >> 3) * 256 + (j >> 4) * 128 + (n & 7) * 16 + (j & 15)] = (unsigned char)(signed char)dig;
+  }
+}
+
+template <int TN>
+__global__ void __launch_bounds__(kI8Threads, 1)
+k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ img, int2* __restrict__ corr,
+               int32_t* __restrict__ lag, int2* __restrict__ val, const __grid_constant__ I8Params p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const I8Smem L = i8_layout(p);
+  const int NB = p.nband, NS = p.nstream, NI = p.nimg;
+  uint64_t* bandfull = reinterpret_cast<uint64_t*>(smem_raw);        // [NB]
+  uint64_t* bandempty = bandfull + 4;                                 // [NB]
+  uint64_t* sfull = bandempty + 4;                                    // [NS]
+  uint64_t* sempty = sfull + 4;                                       // [NS]
+  uint64_t* imgfull = sempty + 4;                                     // [NI]
+  uint64_t* imgempty = imgfull + 4;                                   // [NI]
+  uint64_t* dfull = imgempty + 4;                                     // [2]
+  uint64_t* dempty = dfull + 2;                                       // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + 256);
+  int* dcnt = reinterpret_cast<int*>(smem_raw + 264);                 // [2] digits used per TMEM buffer
+  int* sflag = reinterpret_cast<int*>(smem_raw + 288);                // [4 stages][4 builder warps]
+  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + 384);              // [2][4]
+  int* band = reinterpret_cast<int*>(smem_raw + L.band);
+  unsigned char* stream = smem_raw + L.stream;
+  unsigned char* imgs = smem_raw + L.img;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nterms = p.J + 1;
+  constexpr int NCOL = 32 * TN;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NB; ++i) { mbar_init(&bandfull[i], 1); mbar_init(&bandempty[i], kI8BuildThreads); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], 1); }
+    for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tslot, 2 * kI8BufCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ---------------- loader: band segments (both components) and the term's B images
+    if (lane == 0) {
+      uint32_t u = 0;
+      for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+        for (int step = 0; step < nterms; ++step, ++u) {
+          const I8Term& tm = p.term[step];
+          const uint32_t bs = u % NB, is = u % NI;
+          mbar_wait(&bandempty[bs], ((u / NB) & 1) ^ 1);
+          const uint32_t bytes = (uint32_t)tm.seg_len * 4u;
+          mbar_expect_tx(&bandfull[bs], 2 * bytes);
+          const int* src = bands + ((size_t)row * nterms + tm.band) * 2 * p.stride + tm.seg_a4;
+          int* dst = band + (size_t)bs * 2 * p.seg_alloc;
+          bulk_load_g2s(dst, src, bytes, &bandfull[bs]);
+          bulk_load_g2s(dst + p.seg_alloc, src + p.stride, bytes, &bandfull[bs]);
+          mbar_wait(&imgempty[is], ((u / NI) & 1) ^ 1);
+          const uint32_t ib = (uint32_t)tm.ksteps * 2 * NCOL * 32;
+          mbar_expect_tx(&imgfull[is], ib);
+          bulk_load_g2s(imgs + (size_t)is * p.img_alloc, img + tm.img_ofs, ib, &imgfull[is]);
+        }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      // idesc: D s32, B s8, K-major A and B, N = NCOL, M = 128; A signedness per digit
+      const uint32_t idesc0 = (2u << 4) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const uint32_t st0 = smem_u32(stream), im0 = smem_u32(imgs);
+      uint32_t u = 0, q = 0;
+      for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+        for (int step = 0; step < nterms; ++step, ++u) {
+          const I8Term& tm = p.term[step];
+          const uint32_t ss = u % NS, is = u % NI;
+          mbar_wait(&sfull[ss], (u / NS) & 1);
+          mbar_wait(&imgfull[is], (u / NI) & 1);
+          tc_fence_after();
+          bool fits = true;
+          for (int w = 0; w < kI8BuildWarps; ++w) fits = fits && sflag[ss * 4 + w] != 0;
+          const int D = (fits && tm.dig > 2) ? 2 : tm.dig;
+          for (int t = 0; t < p.ntiles; ++t, ++q) {
+            const uint32_t buf = q & 1;
+            mbar_wait(&dempty[buf], ((q >> 1) & 1) ^ 1);
+            tc_fence_after();
+            dcnt[buf] = D;
+            const uint32_t dt = tmem + buf * kI8BufCols;
+            for (int x = 0; x < 2; ++x)
+              for (int ks = 0; ks < tm.ksteps; ++ks) {
+                const uint64_t bd = smem_desc(im0 + is * p.img_alloc + (ks * 2 + x) * NCOL * 32, 128, 256);
+                for (int b = 0; b < D; ++b) {
+                  const uint32_t a_addr = st0 + ((ss * 2 + x) * p.dmax + b) * p.plane + 2048 * t + ks * tm.kadv;
+                  const uint64_t ad = smem_desc(a_addr, (uint32_t)tm.lbo, 128);
+                  const uint32_t idesc = idesc0 | (b == D - 1 ? (1u << 7) : 0u);
+                  umma_i8(dt + b * NCOL, ad, bd, idesc, (x | ks) ? 1u : 0u);
+                }
+              }
+            umma_commit(&dfull[buf]);
+          }
+          umma_commit(&sempty[ss]);
+          umma_commit(&imgempty[is]);
+        }
+    }
+  } else if (warp < kI8FirstEpi) {
+    // ---------------- builders: int32 band segment -> byte-digit planes (natural order)
+    const int tb = threadIdx.x - 32 * kI8FirstBuild;
+    uint32_t u = 0;
+    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+      for (int step = 0; step < nterms; ++step, ++u) {
+        const I8Term& tm = p.term[step];
+        const uint32_t bs = u % NB, ss = u % NS;
+        mbar_wait(&bandfull[bs], (u / NB) & 1);
+        mbar_wait(&sempty[ss], ((u / NS) & 1) ^ 1);
+        const int nd = tm.dig;
+        const int n4 = tm.seg_len >> 2;
+        unsigned range = 0;
+        for (int x = 0; x < 2; ++x) {
+          const int4* src = reinterpret_cast<const int4*>(band + ((size_t)bs * 2 + x) * p.seg_alloc);
+          unsigned char* dst = stream + ((size_t)ss * 2 + x) * p.dmax * p.plane;
+#pragma unroll 4
+          for (int i = tb; i < n4; i += kI8BuildThreads) {
+            const int4 v = src[i];
+            range |= ((unsigned)v.x + 32768u) | ((unsigned)v.y + 32768u) | ((unsigned)v.z + 32768u) |
+                     ((unsigned)v.w + 32768u);
+            const unsigned p01 = __byte_perm(v.x, v.y, 0x5140), p23 = __byte_perm(v.z, v.w, 0x5140);
+            reinterpret_cast<unsigned*>(dst)[i] = __byte_perm(p01, p23, 0x5410);
+            reinterpret_cast<unsigned*>(dst + p.plane)[i] = __byte_perm(p01, p23, 0x7632);
+            if (nd > 2) {
+              const unsigned q01 = __byte_perm(v.x, v.y, 0x7362), q23 = __byte_perm(v.z, v.w, 0x7362);
+              reinterpret_cast<unsigned*>(dst + 2 * p.plane)[i] = __byte_perm(q01, q23, 0x5410);
+              if (nd > 3) reinterpret_cast<unsigned*>(dst + 3 * p.plane)[i] = __byte_perm(q01, q23, 0x7632);
+            }
+          }
+        }
+        // every staged value in [-32768, 32767]: two digits suffice for this (row, term)
+        const unsigned any_big = __any_sync(0xffffffffu, (range >> 16) != 0u);
+        if (lane == 0) sflag[ss * 4 + (warp - kI8FirstBuild)] = any_big ? 0 : 1;
+        fence_proxy_async_smem();                   // digit planes -> visible to the tensor core
+        mbar_arrive(&sfull[ss]);
+        mbar_arrive(&bandempty[bs]);
+      }
+  } else {
+    // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks
+    const int te = threadIdx.x - 32 * kI8FirstEpi;
+    const int quarter = warp & 3;
+    const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
+    uint32_t q = 0;
+    int par = 0;
+    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
+      unsigned sre[2][16], sim[2][16];                                  // running corr (mod 2^32), per tile
+      for (int step = 0; step < nterms; ++step, par ^= 1) {
+        const int ti = p.J - step;
+        PeakI best;
+        best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (t >= p.ntiles) break;
+          const uint32_t buf = q & 1;
+          mbar_wait(&dfull[buf], (q >> 1) & 1);
+          tc_fence_after();
+          const int D = dcnt[buf];
+          unsigned re[16], im[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) { re[i] = 0u; im[i] = 0u; }
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * kI8BufCols;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            if (b >= D) break;
+#pragma unroll
+            for (int oc = 0; oc < 2; ++oc)
+#pragma unroll
+              for (int a = 0; a < TN; ++a) {
+                uint32_t v[16];
+                tmem_ld16_nowait(tb0 + b * NCOL + oc * 16 * TN + 16 * a, v);
+                tmem_wait_ld16(v);
+                const int sh = 8 * (a + b);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  if (oc == 0) re[i] += v[i] << sh;
+                  else im[i] += v[i] << sh;
+                }
+              }
+          }
+          tc_fence_before();
+          mbar_arrive(&dempty[buf]);
+          ++q;
+          const int tau0 = 2048 * t + 16 * c;
+          if (tau0 < p.N) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (step == 0) { sre[t][i] = re[i]; sim[t][i] = im[i]; }
+              else { sre[t][i] += re[i]; sim[t][i] += im[i]; }
+            }
+            if (p.want_corr) {
+              int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * p.N + tau0);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                dst[i] = make_int4((int)sre[t][2 * i], (int)sim[t][2 * i], (int)sre[t][2 * i + 1], (int)sim[t][2 * i + 1]);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const unsigned long long m = mag2i((int)sre[t][i], (int)sim[t][i]);
+              if (best.tau < 0 || m > best.m2) {
+                best.m2 = m; best.tau = tau0 + i; best.re = (int)sre[t][i]; best.im = (int)sim[t][i];
+              }
+            }
+          }
+        }
+        // the row's peak at scale ti: warp argmax (high word, low word, smallest lag), then 4 warps
+        const bool ok = best.tau >= 0;
+        const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
+        const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
+        const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
+        PeakI* rp = red + par * 4;
+        if (ok && (unsigned)best.tau == tmin) rp[warp - kI8FirstEpi] = best;
+        else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[warp - kI8FirstEpi] = e; }
+        named_bar(2, 128);
+        if (te == 0 && lag) {
+          PeakI b = rp[0];
+          for (int w = 1; w < 4; ++w) {
+            const PeakI o = rp[w];
+            if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
+          }
+          const size_t e = (size_t)row * nterms + ti;
+          lag[e] = b.tau;
+          if (val) val[e] = make_int2(b.re, b.im);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 2 * kI8BufCols);
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+static int digits_for(long long lo, long long hi) {
+  for (int d = 1; d <= 4; ++d) {
+    const long long lim = 1LL << (8 * d - 1);
+    if (lo >= -lim && hi <= lim - 1) return d;
+  }
+  return 5;
+}
+
+bool i8_configure(I8Params& p, int N, int J, int stride, int ML, const int* kmin, const int* cnt, const int* toff,
+                  const int2* taps) {
+  p = I8Params{};
+  if (N % 16 != 0 || N > 4096 || (ML & 3) != 0 || J + 1 > kI8MaxTerms) return false;
+  p.N = N; p.J = J; p.stride = stride; p.ML = ML;
+  p.ntiles = (N + 2047) / 2048;
+  // template digits (balanced, signed): every coefficient and its negation
+  long long tmax = 0;
+  for (int i = 0; i <= J; ++i)
+    for (int k = 0; k < cnt[i]; ++k) {
+      const int2 t = taps[toff[i] + k];
+      tmax = std::max<long long>(tmax, std::max<long long>(std::llabs((long long)t.x), std::llabs((long long)t.y)));
+    }
+  int tn = 1;
+  while (tn <= 4 && tmax > 127LL * ((1LL << (8 * tn)) - 1) / 255) ++tn;
+  if (tn > 4) return false;
+  p.tn = tn; p.ncol = 32 * tn;
+  // static bound of each band from int16 rows through the integer dual program (R-INT):
+  // e += floor((o_k + o_{k-1}) / 2) -> U_s in [2 lo, 2 hi]; o -= floor((e_k + e_{k+1} + 2) / 4) ->
+  // W_s in [lo - hi, hi - lo], (lo, hi) the bound of U_{s-1}
+  long long ulo = -32768, uhi = 32767;
+  int bdig[kI8MaxTerms];
+  for (int s = 1; s <= J; ++s) {
+    bdig[s - 1] = digits_for(ulo - uhi, uhi - ulo);
+    ulo *= 2; uhi *= 2;
+    if (s == J) bdig[J] = digits_for(ulo, uhi);
+  }
+  int dmax = 2, kwin = 0, seg_alloc = 0, img = 0;
+  for (int step = 0; step <= J; ++step) {
+    const int ti = J - step;
+    I8Term& tm = p.term[step];
+    tm.band = ti;
+    tm.lg = ti < J ? ti + 1 : J;
+    tm.kmin = kmin[ti];
+    tm.ntap = cnt[ti];
+    tm.dig = std::max(2, bdig[ti]);
+    if (tm.dig > 4) return false;
+    dmax = std::max(dmax, tm.dig);
+    const int g = 1 << tm.lg;
+    const int gk = g * tm.kmin;
+    tm.strided = g >= 16;
+    if (tm.strided) {
+      tm.sh = 0;
+      tm.P0 = gk;                                            // multiple of 16
+      tm.ksteps = (tm.ntap + 1) / 2;
+      tm.kadv = 2 * g;
+      tm.lbo = g;
+      kwin = std::max(kwin, (tm.ksteps - 1) * 2 * g + g + 16);
+    } else {
+      tm.sh = ((gk + ML) % 4 + 4) % 4;
+      tm.P0 = gk - tm.sh;
+      tm.ksteps = (16 + g * (tm.ntap - 1) + tm.sh + 31) / 32;
+      tm.kadv = 32;
+      tm.lbo = 16;
+      kwin = std::max(kwin, 32 * tm.ksteps);
+    }
+    tm.seg_a4 = tm.P0 + ML;
+    if (tm.seg_a4 < 0 || (tm.seg_a4 & 3) != 0) return false;
+    const long long need = (long long)N + (long long)g * (tm.ntap - 1) + tm.sh + 1;   // stream bytes with nonzero weight
+    const long long have = (long long)stride - tm.seg_a4;
+    tm.seg_len = (int)((std::min(need, have) + 3) & ~3LL);
+    if (tm.seg_len > have) tm.seg_len = (int)(have & ~3LL);
+    seg_alloc = std::max(seg_alloc, tm.seg_len);
+    tm.img_ofs = img;
+    img += tm.ksteps * 2 * p.ncol * 32;
+  }
+  p.dmax = dmax;
+  if (dmax * p.ncol > kI8BufCols) return false;
+  p.seg_alloc = (seg_alloc + 3) & ~3;
+  p.plane = (int)((std::max(2048 * p.ntiles - 16 + kwin, seg_alloc) + 127) & ~127);
+  int img_alloc = 0;
+  for (int step = 0; step <= J; ++step) img_alloc = std::max(img_alloc, p.term[step].ksteps * 2 * p.ncol * 32);
+  p.img_alloc = (img_alloc + 127) & ~127;
+  p.nstream = 2;
+  p.nimg = 2;
+  const size_t budget = 227 * 1024;
+  for (p.nband = 4; p.nband >= 2; --p.nband)
+    if (i8_layout(p).total <= budget) break;
+  if (i8_layout(p).total > budget) return false;
+  return true;
+}
+
+size_t i8_image_bytes(const I8Params& p) {
+  size_t b = 0;
+  for (int step = 0; step <= p.J; ++step) b += (size_t)p.term[step].ksteps * 2 * p.ncol * 32;
+  return b;
+}
+
+size_t i8_smem_bytes(const I8Params& p) { return i8_layout(p).total; }
+
+cudaError_t i8_build_images(const I8Params& p, const int2* d_taps, const int* toff, unsigned char* d_img) {
+  int total_ks = 0;
+  for (int step = 0; step <= p.J; ++step) total_ks += p.term[step].ksteps;
+  int* d_toff = nullptr;
+  cudaError_t e = cudaMalloc(&d_toff, kI8MaxTerms * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpy(d_toff, toff, (p.J + 1) * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    const int total = total_ks * 2 * p.ncol;
+    k_i8_images<<<(total + 127) / 128, 128>>>(d_taps, p, d_toff, total, d_img);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (d_toff) cudaFree(d_toff);
+  return e;
+}
+
+cudaError_t i8_launch(const I8Params& p, const int* bands, const unsigned char* img, int2* corr, int32_t* lag,
+                      int2* val, int grid, cudaStream_t s) {
+  const size_t smem = i8_layout(p).total;
+  void (*kern)(const int*, const unsigned char*, int2*, int32_t*, int2*, const I8Params);
+  switch (p.tn) {
+    case 1: kern = k_correlate_i8<1>; break;
+    case 2: kern = k_correlate_i8<2>; break;
+    case 3: kern = k_correlate_i8<3>; break;
+    default: kern = k_correlate_i8<4>; break;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kI8Threads, smem, s>>>(bands, img, corr, lag, val, p);
+  return cudaGetLastError();
+}
+
+}  // namespace sidwt

@@ -150,6 +150,7 @@ __device__ __forceinline__ void split_bf16(float v, float& hi, float& lo) {
 // lags, and the template rows of a quarter-warp differ in bit 2 (conflict-free swizzled
 // staging stores).
 // ---------------------------------------------------------------------------
+#ifndef SIDWT_NO_KERNELS
 __global__ void k_tc_images(const float2* __restrict__ taps, int taps_per_t, TcParams p, unsigned char* __restrict__ img) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)p.n_mt * p.total_ksteps * 2 * kTcM;
@@ -182,6 +183,8 @@ __global__ void k_tc_images(const float2* __restrict__ taps, int taps_per_t, TcP
     *reinterpret_cast<__nv_bfloat16*>(blk + off) = out;
   }
 }
+
+#endif  // SIDWT_NO_KERNELS
 
 // ---------------------------------------------------------------------------
 // The bank correlation kernel: persistent, warp-specialised, one CTA per SM.
@@ -308,6 +311,7 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t sa
                :: "l"(map), "r"(saddr), "r"(x0), "r"(x1), "r"(x2), "r"(x3) : "memory");
 }
 
+#ifndef SIDWT_NO_KERNELS
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict__ img, float2* __restrict__ corr,
                PeakF* __restrict__ partials, const __grid_constant__ TcParams p) {
@@ -696,5 +700,7 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
     tmem_dealloc(tbase, 512);
   }
 }
+
+#endif  // SIDWT_NO_KERNELS
 
 }  // namespace sidwt

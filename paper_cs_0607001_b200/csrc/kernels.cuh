@@ -90,7 +90,7 @@ __device__ void analysis_level(int fam, const Lift64& L, const V* cur, long lo, 
   }
 }
 
-__device__ void analysis_level_int(const int64_t* cur, long lo, long hi, int64_t* e, int64_t* o, long klo, long khi) {
+__device__ inline void analysis_level_int(const int64_t* cur, long lo, long hi, int64_t* e, int64_t* o, long klo, long khi) {
   for (long k = klo; k <= khi; ++k) {
     e[k - klo] = getz(cur, lo, hi, 2 * k);
     o[k - klo] = getz(cur, lo, hi, 2 * k + 1);
@@ -104,6 +104,7 @@ __device__ void analysis_level_int(const int64_t* cur, long lo, long hi, int64_t
 __host__ __device__ inline long fl_div2(long a) { return a >= 0 ? a / 2 : -((-a + 1) / 2); }
 __host__ __device__ inline long cl_div2(long a) { return -fl_div2(-a); }
 
+#ifndef SIDWT_NO_KERNELS   // non-template kernels: defined in the one TU that launches them (sidwt.cu)
 // table: [n_t][taps_per_t] float2 (or int2); scratch: per thread 4 * scratch_len values
 // nres > 1 (the paper's orientation, template carries the redundant tree): thread residue
 // rho pyramids the template delayed by rho (support [rho, rho + T)); term i keeps the
@@ -168,6 +169,8 @@ __global__ void k_template_pyramid(const void* __restrict__ x, void* __restrict_
     for (int i = 0; i < p.cnt[p.J]; ++i) tab[2 * (p.off[p.J] + i) + comp] = (int)cur[p.klo[p.J] + i - lo];
   }
 }
+
+#endif  // SIDWT_NO_KERNELS
 
 // ---------------------------------------------------------------------------
 // K1: fused multi-level SIDWT lifting of one (row, component, tile).

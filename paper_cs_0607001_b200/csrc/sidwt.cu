@@ -18,6 +18,7 @@
 #include "corr_tc.cuh"
 #include "corr_tcs.cuh"
 #include "fused.cuh"
+#include "corr_i8.h"
 
 using namespace sidwt;
 
@@ -89,6 +90,9 @@ struct sidwt_plan_s {
   void* d_tcs_img = nullptr;
   size_t tcs_smem = 0;
   int tcs_total_ksteps = 0;
+  bool i8 = false;                   // integer family on the int8 tensor cores (corr_i8.cu)
+  I8Params i8p{};
+  void* d_i8_img = nullptr;
 };
 
 static bool is_int(const sidwt_plan_s* p) { return p->fam == SIDWT_LEGALL53_INT; }
@@ -128,7 +132,7 @@ sidwt_status sidwt_plan_create(sidwt_plan* out, int filter, int levels, int64_t 
 
 static void free_ws(sidwt_plan_s* p) {
   void** bufs[] = {&p->d_taps, &p->d_partials, &p->w_rows, &p->w_bands, &p->w_lag, &p->w_val, &p->d_img,
-                   &p->d_tcs_img};
+                   &p->d_tcs_img, &p->d_i8_img};
   for (void** b : bufs) { if (*b) cudaFree(*b); *b = nullptr; }
   p->w_rows_bytes = p->w_bands_bytes = p->w_lag_bytes = p->w_val_bytes = 0;
   for (cudaEvent_t& ev : p->ev) { if (ev) cudaEventDestroy(ev); ev = nullptr; }
@@ -177,7 +181,9 @@ int64_t sidwt_corr_bytes(sidwt_plan p, int64_t rows) {
   return rows * p->n_t * (p->J + 1) * p->N * 8;
 }
 int sidwt_last_launches(sidwt_plan p) { return p ? p->last_launches : 0; }
-int sidwt_uses_tensor_cores(sidwt_plan p) { return (p && p->loaded) ? (p->tc ? 1 : (p->tcs ? 2 : 0)) : -1; }
+int sidwt_uses_tensor_cores(sidwt_plan p) {
+  return (p && p->loaded) ? (p->tc ? 1 : (p->tcs ? 2 : (p->i8 ? 3 : 0))) : -1;
+}
 int sidwt_template_is_real(sidwt_plan p) { return (p && p->loaded) ? (p->real_taps ? 1 : 0) : -1; }
 
 // ---------------------------------------------------------------------------
@@ -231,6 +237,7 @@ static void configure(sidwt_plan_s* p) {
   } else {
     ML = std::max(ML, 1 << J);
   }
+  if (is_int(p)) ML = (int)rup(ML, 4);      // int8 tensor-core path: 16-byte aligned band segments
   if (p->ext == SIDWT_EXT_PERIODIC) { ML = 0; MR = 0; }
   p->ML = ML; p->MR = MR;
   p->stride = rup(ML + p->N + MR, 32);
@@ -418,6 +425,21 @@ static void configure_tcs(sidwt_plan_s* p) {
   p->tcs = true;
 }
 
+// Integer family on the int8 tensor cores (corr_i8.cu): one template, symmetric extension,
+// N <= 4096 (two 2048-lag tiles per row).  SIDWT_I8=0 disables it (the INT32 SIMT kernel runs).
+static void configure_i8(sidwt_plan_s* p) {
+  p->i8 = false;
+  const char* env = std::getenv("SIDWT_I8");
+  if (env && env[0] == '0') return;
+  if (!is_int(p) || p->n_t != 1 || p->ext != SIDWT_EXT_SYMMETRIC || p->paper) return;
+  std::vector<int2> taps((size_t)p->taps_per_t);
+  if (cudaMemcpy(taps.data(), p->d_taps, taps.size() * sizeof(int2), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  p->i8 = i8_configure(p->i8p, (int)p->N, p->J, (int)p->stride, p->ML, p->kmin, p->cnt, p->toff, taps.data());
+}
+
 // Fused path: single template, taps in the kernel parameters, and a
 // tile whose on-chip bands + term results fit two CTAs per SM.
 constexpr int kFusNT = 256;
@@ -494,6 +516,7 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   if (p->d_partials) { cudaFree(p->d_partials); p->d_partials = nullptr; p->partials_bytes = 0; }
   if (p->d_img) { cudaFree(p->d_img); p->d_img = nullptr; }
   if (p->d_tcs_img) { cudaFree(p->d_tcs_img); p->d_tcs_img = nullptr; }
+  if (p->d_i8_img) { cudaFree(p->d_i8_img); p->d_i8_img = nullptr; }
   p->loaded = false;
   p->T = (int)T; p->n_t = n_templates;
   configure(p);
@@ -543,6 +566,17 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
   configure_fused(p);
   configure_tc(p);
   configure_tcs(p);
+  configure_i8(p);
+  if (p->i8) {
+    e = cudaMalloc(&p->d_i8_img, i8_image_bytes(p->i8p));
+    if (e == cudaSuccess) e = i8_build_images(p->i8p, static_cast<const int2*>(p->d_taps), p->toff,
+                                              static_cast<unsigned char*>(p->d_i8_img));
+    if (e != cudaSuccess) {
+      if (p->d_i8_img) { cudaFree(p->d_i8_img); p->d_i8_img = nullptr; }
+      cudaFree(p->d_taps); p->d_taps = nullptr;
+      return cuda_status(e);
+    }
+  }
 
   if (p->tcs) {
     const size_t img_bytes = (size_t)p->tcs_total_ksteps * kTcsAStage;
@@ -711,9 +745,26 @@ static sidwt_status correlate_tcs(sidwt_plan_s* p, const void* d_bands, int64_t 
   return cuda_status(e);
 }
 
+static sidwt_status correlate_i8(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
+                                 int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
+  I8Params t = p->i8p;
+  t.rows = rows;
+  t.want_corr = d_corr != nullptr;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(rows, sms);
+  cudaError_t e = i8_launch(t, static_cast<const int*>(d_bands), static_cast<const unsigned char*>(p->d_i8_img),
+                            static_cast<int2*>(d_corr), peaks ? d_lag : nullptr,
+                            peaks ? static_cast<int2*>(d_val) : nullptr, grid, s);
+  p->last_launches = 1;
+  return cuda_status(e);
+}
+
 static sidwt_status correlate_impl(sidwt_plan_s* p, const void* d_bands, int64_t rows, void* d_corr,
                                    int32_t* d_lag, void* d_val, bool peaks, cudaStream_t s) {
   if (p->tc) return correlate_tc(p, d_bands, rows, d_corr, d_lag, d_val, peaks, s);
+  if (p->i8) return correlate_i8(p, d_bands, rows, d_corr, d_lag, d_val, peaks, s);
   if (p->tcs) return correlate_tcs(p, d_bands, rows, d_corr, d_lag, d_val, peaks, s);
   CorParams c = p->cor;
   c.rows = rows;

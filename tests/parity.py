@@ -41,8 +41,10 @@ def oracle_for(plan, rows, templates, corr=True, nthreads=0):
                  corr=corr, nthreads=nthreads)
 
 
-def compare(plan, g, r, row_ids=None, check_bands=True):
+def compare(plan, g, r, row_ids=None, check_bands=True, neartie_bound=False):
     """Assert parity of gpu result g (possibly for a superset of rows) with oracle r.
+    neartie_bound: the BASELINE workloads (not degenerate edge cases, whose coarse scales
+    can tie exactly) must have R3 near-tie accepts on at most NEARTIE_FRAC of the lags.
     Returns stats dict."""
     J = plan.levels
     stats = dict(band_rel_l2=0.0, corr_err=0.0, lag_exact=0, lag_neartie=0)
@@ -99,7 +101,8 @@ def compare(plan, g, r, row_ids=None, check_bands=True):
     stats["lag_total"] = int(gl.size)
     # R3 is a safety net: exact lag agreement is expected (no top-two
     # gap below 1e-5 in 20 000 C3-like rows), so near ties must stay rare
-    assert stats["lag_neartie"] <= max(1, int(np.ceil(NEARTIE_FRAC * gl.size))), stats
+    if neartie_bound:
+        assert stats["lag_neartie"] <= max(1, int(np.ceil(NEARTIE_FRAC * gl.size))), stats
     # peak values: value of the GPU's corr at the GPU's lag
     gvc = gv[..., 0] + 1j * gv[..., 1]
     picked = np.take_along_axis(gcc, gl[..., None].astype(np.int64), -1)[..., 0]

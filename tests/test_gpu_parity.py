@@ -46,7 +46,7 @@ def test_config_small(cid, nrows, fused):
     _taps_match(plan, tm)
     g = run_gpu(plan, rows, fused=fused)
     r = oracle_for(plan, rows, tm)
-    st = compare(plan, g, r)
+    st = compare(plan, g, r, neartie_bound=True)
     print(cfg.name, st)
 
 
@@ -181,7 +181,7 @@ def test_full_size_sampled(cid):
     g = dict(bands=bands.index_select(0, it).cpu().numpy(), corr=corr.index_select(0, it).cpu().numpy(),
              lag=lag.index_select(0, it).cpu().numpy(), val=val.index_select(0, it).cpu().numpy())
     r = oracle_for(plan, rows[ids], tm)
-    st = compare(plan, g, r)
+    st = compare(plan, g, r, neartie_bound=True)
     assert st["lag_total"] == 256 * (cfg.levels + 1)
     # property at any size: every lag is in range
     lg = lag.cpu().numpy()
@@ -211,7 +211,7 @@ def test_full_size_c4_sampled():
              lag=lag.index_select(0, it).cpu().numpy(), val=val.index_select(0, it).cpu().numpy())
     assert np.array_equal(g["lag"], sub[1].cpu().numpy())       # peaks-only == with-corr peaks
     r = oracle_for(plan, rows[ids], tm)
-    st = compare(plan, g, r)
+    st = compare(plan, g, r, neartie_bound=True)
     assert st["lag_total"] == 16 * 64 * (cfg.levels + 1)
     print(cfg.name, "full-size, 16 pulses x 64 templates vs oracle", st)
 
