@@ -51,7 +51,9 @@ constexpr int kI8Warps = 10;
 constexpr int kI8Threads = 32 * kI8Warps;
 constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6;
 constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
-constexpr int kI8BufCols = 256;                     // TMEM columns per accumulator buffer (dmax * ncol <= 256)
+// TMEM: 512 columns, two accumulator buffers of 256 (tile t+1's MMAs overlap tile t's epilogue)
+// when dmax * ncol <= 256, else one buffer of 512
+constexpr int kI8TmemCols = 512;
 
 struct I8Smem { size_t band, stream, img, total; };
 __host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
@@ -164,7 +166,9 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 128); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tslot, 2 * kI8BufCols);
+  if (warp == 1) tmem_alloc(tslot, kI8TmemCols);
+  const int NBUF = p.dmax * NCOL <= kI8TmemCols / 2 ? 2 : 1;
+  const uint32_t bufcols = kI8TmemCols / NBUF;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -209,11 +213,11 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           for (int w = 0; w < kI8BuildWarps; ++w) fits = fits && sflag[ss * 4 + w] != 0;
           const int D = (fits && tm.dig > 2) ? 2 : tm.dig;
           for (int t = 0; t < p.ntiles; ++t, ++q) {
-            const uint32_t buf = q & 1;
-            mbar_wait(&dempty[buf], ((q >> 1) & 1) ^ 1);
+            const uint32_t buf = q % NBUF;
+            mbar_wait(&dempty[buf], ((q / NBUF) & 1) ^ 1);
             tc_fence_after();
             dcnt[buf] = D;
-            const uint32_t dt = tmem + buf * kI8BufCols;
+            const uint32_t dt = tmem + buf * bufcols;
             for (int x = 0; x < 2; ++x)
               for (int ks = 0; ks < tm.ksteps; ++ks) {
                 const uint64_t bd = smem_desc(im0 + is * p.img_alloc + (ks * 2 + x) * NCOL * 32, 128, 256);
@@ -284,14 +288,14 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if (t >= p.ntiles) break;
-          const uint32_t buf = q & 1;
-          mbar_wait(&dfull[buf], (q >> 1) & 1);
+          const uint32_t buf = q % NBUF;
+          mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
           const int D = dcnt[buf];
           unsigned re[16], im[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) { re[i] = 0u; im[i] = 0u; }
-          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * kI8BufCols;
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             if (b >= D) break;
@@ -361,7 +365,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 2 * kI8BufCols);
+  if (warp == 1) tmem_dealloc(tmem, kI8TmemCols);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,7 +446,7 @@ bool i8_configure(I8Params& p, int N, int J, int stride, int ML, const int* kmin
     img += tm.ksteps * 2 * p.ncol * 32;
   }
   p.dmax = dmax;
-  if (dmax * p.ncol > kI8BufCols) return false;
+  if (dmax * p.ncol > kI8TmemCols) return false;
   p.seg_alloc = (seg_alloc + 3) & ~3;
   p.plane = (int)((std::max(2048 * p.ntiles - 16 + kwin, seg_alloc) + 127) & ~127);
   int img_alloc = 0;
