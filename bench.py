@@ -465,8 +465,19 @@ def main():
     k2_tflops = R * alg["k2_flops"] / (k2_ms * 1e-3) / 1e12
     k2_gbs = R * alg["k2_bytes"] / (k2_ms * 1e-3) / 1e9
     fp32_peak = fp32_peak_tflops(pk["sm_mhz"])
-    k2_kernel = ("k_correlate", "k_correlate_tc", "k_correlate_tcs")[tc_path]
-    if tc:
+    k2_kernel = ("k_correlate", "k_correlate_tc", "k_correlate_tcs", "k_correlate_i8")[tc_path]
+    if tc_path == 3:
+        # int8 tensor pipe (exact digit GEMM): algorithmic integer ops (4 multiplies + 4 adds per
+        # complex MAC) against the int8 dense peak = measured sustained bf16 x the nominal
+        # int8 / bf16 ratio (4.5 / 2.25 PFLOP/s, B200_PROFILING.md)
+        i8_peak = 2.0 * pk["bf16_sustained"]
+        comp = {"achieved": k2_tflops, "peak": i8_peak, "unit": "Tops/s (int8 tensor)", "frac": k2_tflops / i8_peak,
+                "flops_per_row": alg["k2_flops"],
+                "note": "algorithmic int ops of the complex MACs; the kernel issues 4 real products x "
+                        "(2 or 3 data digits) x (template digits) int8 MACs per complex MAC",
+                "peak_source": f"{pk['src']} MEASURED_PEAKS.json bf16_tflops_sustained x 2 (int8/bf16 nominal ratio)"}
+        comp_key, comp_bound = "tensor", "tensor"
+    elif tc:
         # tensor pipe: the algorithmic complex MACs run as 3 bf16 products (split precision);
         # peak = measured sustained cuBLAS bf16 (the kernel runs inside a long power-capped step)
         comp = {"achieved": k2_tflops * BF16_SPLIT_PRODUCTS, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
@@ -489,7 +500,7 @@ def main():
     stages = {
         "analyze": {"kernel": "k_analyze", "ms": k1_ms, "bound": "hbm", "achieved": k1_gbs, "peak": pk["hbm"],
                     "unit": "GB/s", "frac": k1_gbs / pk["hbm"], "bytes_per_row": alg["k1_bytes"]},
-        "correlate_peaks": {"kernel": k2_kernel + ("" if tc_path == 2 else "+k_peaks_finalize"), "ms": k2_ms,
+        "correlate_peaks": {"kernel": k2_kernel + ("" if tc_path in (2, 3) else "+k_peaks_finalize"), "ms": k2_ms,
                             comp_key: comp,
                             "hbm": {"achieved": k2_gbs, "peak": pk["hbm"], "unit": "GB/s",
                                     "frac": k2_gbs / pk["hbm"], "bytes_per_row": alg["k2_bytes"]}},

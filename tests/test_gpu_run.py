@@ -43,7 +43,7 @@ def test_run_equals_two_call_path(cid, nrows, chunks):
     assert np.array_equal(b, g["bands"]), "run: bands differ from sidwt_analyze"
     assert np.array_equal(c, g["corr"]), "run: corr differs from the two-call path"
     assert np.array_equal(l, g["lag"]) and np.array_equal(v, g["val"])
-    per_chunk = 2 if plan.tensor_core_path() == 2 else 3        # analyze + correlate (+ peak finalize)
+    per_chunk = 2 if plan.tensor_core_path() in (2, 3) else 3        # analyze + correlate (+ peak finalize)
     assert launches == per_chunk * min(chunks, nrows)
     _, _, pl, pv, _ = _run(plan, rows, chunks, want_corr=False)         # peaks only
     assert np.array_equal(pl, g["lag"]) and np.array_equal(pv, g["val"])
