@@ -47,9 +47,9 @@
 
 namespace sidwt {
 
-constexpr int kI8Warps = 10;
+constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6, kI8EpiWarps = 8;
+constexpr int kI8Warps = kI8FirstEpi + kI8EpiWarps;
 constexpr int kI8Threads = 32 * kI8Warps;
-constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6;
 constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
 // TMEM: 512 columns, two accumulator buffers of 256 (tile t+1's MMAs overlap tile t's epilogue)
 // when dmax * ncol <= 256, else one buffer of 512
@@ -74,6 +74,21 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
       :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
 }
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n" : "=r"(pred));
+  return pred != 0;
+}
+
+// 32 lanes x 8 consecutive 32-bit columns -> 8 registers per thread (no wait); the wait for all
+// of a thread's outstanding loads is tmem_wait_ld_all (memory clobber orders the uses)
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld_all() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread (no wait)
 __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
@@ -151,7 +166,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + 256);
   int* dcnt = reinterpret_cast<int*>(smem_raw + 264);                 // [2] digits used per TMEM buffer
   int* sflag = reinterpret_cast<int*>(smem_raw + 288);                // [4 stages][4 builder warps]
-  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + 384);              // [2][4]
+  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + 384);              // [2][kI8EpiWarps]
   int* band = reinterpret_cast<int*>(smem_raw + L.band);
   unsigned char* stream = smem_raw + L.stream;
   unsigned char* imgs = smem_raw + L.img;
@@ -163,7 +178,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     for (int i = 0; i < NB; ++i) { mbar_init(&bandfull[i], 1); mbar_init(&bandempty[i], kI8BuildThreads); }
     for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], 1); }
     for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 128); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * kI8EpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tslot, kI8TmemCols);
@@ -196,44 +211,55 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      // idesc: D s32, B s8, K-major A and B, N = NCOL, M = 128; A signedness per digit
-      const uint32_t idesc0 = (2u << 4) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-      const uint32_t st0 = smem_u32(stream), im0 = smem_u32(imgs);
-      uint32_t u = 0, q = 0;
-      for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
-        for (int step = 0; step < nterms; ++step, ++u) {
-          const I8Term& tm = p.term[step];
-          const uint32_t ss = u % NS, is = u % NI;
-          mbar_wait(&sfull[ss], (u / NS) & 1);
-          mbar_wait(&imgfull[is], (u / NI) & 1);
+    // ---------------- MMA issuer: the whole warp runs the loop (uniform values stay in uniform
+    // registers), one elected lane issues the MMAs and their commits
+    const uint32_t idesc0 = (2u << 4) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t st0 = smem_u32(stream), im0 = smem_u32(imgs);
+    const uint32_t plane16 = (uint32_t)p.plane >> 4;
+    uint32_t u = 0, q = 0;
+    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+      for (int step = 0; step < nterms; ++step, ++u) {
+        const int ksteps = p.term[step].ksteps, kadv16 = p.term[step].kadv >> 4, dig = p.term[step].dig;
+        const uint32_t ss = u % NS, is = u % NI;
+        mbar_wait(&sfull[ss], (u / NS) & 1);
+        mbar_wait(&imgfull[is], (u / NI) & 1);
+        tc_fence_after();
+        bool fits = true;
+        for (int w = 0; w < kI8BuildWarps; ++w) fits = fits && sflag[ss * 4 + w] != 0;
+        const int D = (fits && dig > 2) ? 2 : dig;
+        // A signedness: the top digit signed, the others unsigned
+        const uint32_t id0 = idesc0 | (D == 1 ? (1u << 7) : 0u), id1 = idesc0 | (D == 2 ? (1u << 7) : 0u);
+        const uint32_t id2 = idesc0 | (D == 3 ? (1u << 7) : 0u), id3 = idesc0 | (1u << 7);
+        const uint64_t bdesc0 = smem_desc(im0 + is * p.img_alloc, 128, 256);
+        const uint64_t adesc0 = smem_desc(st0 + ss * 2 * p.dmax * p.plane, (uint32_t)p.term[step].lbo, 128);
+        for (int t = 0; t < p.ntiles; ++t, ++q) {
+          const uint32_t buf = q % NBUF;
+          mbar_wait(&dempty[buf], ((q / NBUF) & 1) ^ 1);
           tc_fence_after();
-          bool fits = true;
-          for (int w = 0; w < kI8BuildWarps; ++w) fits = fits && sflag[ss * 4 + w] != 0;
-          const int D = (fits && tm.dig > 2) ? 2 : tm.dig;
-          for (int t = 0; t < p.ntiles; ++t, ++q) {
-            const uint32_t buf = q % NBUF;
-            mbar_wait(&dempty[buf], ((q / NBUF) & 1) ^ 1);
-            tc_fence_after();
-            dcnt[buf] = D;
-            const uint32_t dt = tmem + buf * bufcols;
+          if (lane == 0) dcnt[buf] = D;
+          __syncwarp();
+          const uint32_t dt = tmem + buf * bufcols;
+          if (elect_one()) {
             for (int x = 0; x < 2; ++x)
-              for (int ks = 0; ks < tm.ksteps; ++ks) {
-                const uint64_t bd = smem_desc(im0 + is * p.img_alloc + (ks * 2 + x) * NCOL * 32, 128, 256);
-                for (int b = 0; b < D; ++b) {
-                  const uint32_t a_addr = st0 + ((ss * 2 + x) * p.dmax + b) * p.plane + 2048 * t + ks * tm.kadv;
-                  const uint64_t ad = smem_desc(a_addr, (uint32_t)tm.lbo, 128);
-                  const uint32_t idesc = idesc0 | (b == D - 1 ? (1u << 7) : 0u);
-                  umma_i8(dt + b * NCOL, ad, bd, idesc, (x | ks) ? 1u : 0u);
-                }
+              for (int ks = 0; ks < ksteps; ++ks) {
+                const uint64_t bd = bdesc0 + (uint64_t)((ks * 2 + x) * (NCOL * 2));
+                const uint64_t ad = adesc0 + (uint64_t)(x * p.dmax * plane16 + 128 * t + ks * kadv16);
+                const uint32_t acc = (x | ks) ? 1u : 0u;
+                umma_i8(dt, ad, bd, id0, acc);
+                if (D > 1) umma_i8(dt + NCOL, ad + plane16, bd, id1, acc);
+                if (D > 2) umma_i8(dt + 2 * NCOL, ad + 2 * plane16, bd, id2, acc);
+                if (D > 3) umma_i8(dt + 3 * NCOL, ad + 3 * plane16, bd, id3, acc);
               }
             umma_commit(&dfull[buf]);
           }
+          __syncwarp();
+        }
+        if (elect_one()) {
           umma_commit(&sempty[ss]);
           umma_commit(&imgempty[is]);
         }
-    }
+        __syncwarp();
+      }
   } else if (warp < kI8FirstEpi) {
     // ---------------- builders: int32 band segment -> byte-digit planes (natural order)
     const int tb = threadIdx.x - 32 * kI8FirstBuild;
@@ -273,14 +299,15 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         mbar_arrive(&bandempty[bs]);
       }
   } else {
-    // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks
+    // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
+    // Two warps per TMEM lane quarter; warp half h takes shifts p = 8h .. 8h+7 of every lag block.
     const int te = threadIdx.x - 32 * kI8FirstEpi;
-    const int quarter = warp & 3;
+    const int quarter = warp & 3, h = (warp - kI8FirstEpi) >> 2;
     const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
     uint32_t q = 0;
     int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      unsigned sre[2][16], sim[2][16];                                  // running corr (mod 2^32), per tile
+      unsigned sre[2][8], sim[2][8];                                    // running corr (mod 2^32), per tile
       for (int step = 0; step < nterms; ++step, par ^= 1) {
         const int ti = p.J - step;
         PeakI best;
@@ -292,46 +319,55 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
           const int D = dcnt[buf];
-          unsigned re[16], im[16];
+          unsigned re[8], im[8];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) { re[i] = 0u; im[i] = 0u; }
-          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols;
+          for (int i = 0; i < 8; ++i) { re[i] = 0u; im[i] = 0u; }
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + 8 * h;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             if (b >= D) break;
+            uint32_t v[2][TN][8];                                       // every load of digit b, one wait
+#pragma unroll
+            for (int oc = 0; oc < 2; ++oc)
+#pragma unroll
+              for (int a = 0; a < TN; ++a) tmem_ld8_nowait(tb0 + b * NCOL + oc * 16 * TN + 16 * a, v[oc][a]);
+            tmem_wait_ld_all();
+#pragma unroll
+            for (int oc = 0; oc < 2; ++oc)
+#pragma unroll
+              for (int a = 0; a < TN; ++a)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) asm volatile("" : "+r"(v[oc][a][i]));   // uses after the wait
 #pragma unroll
             for (int oc = 0; oc < 2; ++oc)
 #pragma unroll
               for (int a = 0; a < TN; ++a) {
-                uint32_t v[16];
-                tmem_ld16_nowait(tb0 + b * NCOL + oc * 16 * TN + 16 * a, v);
-                tmem_wait_ld16(v);
                 const int sh = 8 * (a + b);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  if (oc == 0) re[i] += v[i] << sh;
-                  else im[i] += v[i] << sh;
+                for (int i = 0; i < 8; ++i) {
+                  if (oc == 0) re[i] += v[oc][a][i] << sh;
+                  else im[i] += v[oc][a][i] << sh;
                 }
               }
           }
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
           ++q;
-          const int tau0 = 2048 * t + 16 * c;
+          const int tau0 = 2048 * t + 16 * c + 8 * h;
           if (tau0 < p.N) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < 8; ++i) {
               if (step == 0) { sre[t][i] = re[i]; sim[t][i] = im[i]; }
               else { sre[t][i] += re[i]; sim[t][i] += im[i]; }
             }
             if (p.want_corr) {
               int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * p.N + tau0);
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
+              for (int i = 0; i < 4; ++i)
                 dst[i] = make_int4((int)sre[t][2 * i], (int)sim[t][2 * i], (int)sre[t][2 * i + 1], (int)sim[t][2 * i + 1]);
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < 8; ++i) {
               const unsigned long long m = mag2i((int)sre[t][i], (int)sim[t][i]);
               if (best.tau < 0 || m > best.m2) {
                 best.m2 = m; best.tau = tau0 + i; best.re = (int)sre[t][i]; best.im = (int)sim[t][i];
@@ -339,20 +375,20 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
             }
           }
         }
-        // the row's peak at scale ti: warp argmax (high word, low word, smallest lag), then 4 warps
+        // the row's peak at scale ti: warp argmax (high word, low word, smallest lag), then 8 warps
         const bool ok = best.tau >= 0;
         const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
         const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
         const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
         const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
         const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
-        PeakI* rp = red + par * 4;
+        PeakI* rp = red + par * kI8EpiWarps;
         if (ok && (unsigned)best.tau == tmin) rp[warp - kI8FirstEpi] = best;
         else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[warp - kI8FirstEpi] = e; }
-        named_bar(2, 128);
+        named_bar(2, 32 * kI8EpiWarps);
         if (te == 0 && lag) {
           PeakI b = rp[0];
-          for (int w = 1; w < 4; ++w) {
+          for (int w = 1; w < kI8EpiWarps; ++w) {
             const PeakI o = rp[w];
             if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
           }
