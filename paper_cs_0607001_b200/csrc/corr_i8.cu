@@ -42,6 +42,8 @@
 #include "corr_tc.cuh"
 #include "corr_i8.h"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -55,15 +57,24 @@ constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
 // when dmax * ncol <= 256, else one buffer of 512
 constexpr int kI8TmemCols = 512;
 
-struct I8Smem { size_t band, stream, img, total; };
+struct I8Smem { size_t red, stg, band, stream, img, total; };
+constexpr int kI8StgBytes = 2048;                   // per epilogue warp and buffer: 32 lag blocks x 8 lags x 8 B
 __host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
   I8Smem L;
-  L.band = 1024;                                                        // barriers, flags, peak partials below
+  L.red = 1024;                                                         // [2 rows][J+1][kI8EpiWarps] peak partials
+  L.stg = (L.red + (size_t)2 * kI8MaxTerms * kI8EpiWarps * 24 + 1023) & ~(size_t)1023;   // 64B-swizzled TMA staging
+  L.band = L.stg + (size_t)kI8EpiWarps * 2 * kI8StgBytes;
   L.stream = (L.band + (size_t)p.nband * 2 * p.seg_alloc * 4 + 127) & ~(size_t)127;
   L.img = L.stream + (size_t)p.nstream * 2 * p.dmax * p.plane;
   L.total = L.img + (size_t)p.nimg * p.img_alloc;
   return L;
 }
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t saddr, int x0, int x1, int x2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n"
+               :: "l"(map), "r"(saddr), "r"(x0), "r"(x1), "r"(x2) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
 
 // D[tmem] (+)= A[smem] . B[smem], kind::i8 (int8 inputs, int32 accumulate)
 __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -166,7 +177,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + 256);
   int* dcnt = reinterpret_cast<int*>(smem_raw + 264);                 // [2] digits used per TMEM buffer
   int* sflag = reinterpret_cast<int*>(smem_raw + 288);                // [4 stages][4 builder warps]
-  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + 384);              // [2][kI8EpiWarps]
+  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + L.red);            // [2][kI8MaxTerms][kI8EpiWarps]
+  unsigned char* stg = smem_raw + L.stg;                              // [kI8EpiWarps][2][kI8StgBytes]
   int* band = reinterpret_cast<int*>(smem_raw + L.band);
   unsigned char* stream = smem_raw + L.stream;
   unsigned char* imgs = smem_raw + L.img;
@@ -273,27 +285,52 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         const int nd = tm.dig;
         const int n4 = tm.seg_len >> 2;
         unsigned range = 0;
+        // pass 1: digit planes 0 and 1 and the range of the staged values (4 loads in flight)
         for (int x = 0; x < 2; ++x) {
-          const int4* src = reinterpret_cast<const int4*>(band + ((size_t)bs * 2 + x) * p.seg_alloc);
-          unsigned char* dst = stream + ((size_t)ss * 2 + x) * p.dmax * p.plane;
-#pragma unroll 4
-          for (int i = tb; i < n4; i += kI8BuildThreads) {
-            const int4 v = src[i];
-            range |= ((unsigned)v.x + 32768u) | ((unsigned)v.y + 32768u) | ((unsigned)v.z + 32768u) |
-                     ((unsigned)v.w + 32768u);
-            const unsigned p01 = __byte_perm(v.x, v.y, 0x5140), p23 = __byte_perm(v.z, v.w, 0x5140);
-            reinterpret_cast<unsigned*>(dst)[i] = __byte_perm(p01, p23, 0x5410);
-            reinterpret_cast<unsigned*>(dst + p.plane)[i] = __byte_perm(p01, p23, 0x7632);
-            if (nd > 2) {
-              const unsigned q01 = __byte_perm(v.x, v.y, 0x7362), q23 = __byte_perm(v.z, v.w, 0x7362);
-              reinterpret_cast<unsigned*>(dst + 2 * p.plane)[i] = __byte_perm(q01, q23, 0x5410);
-              if (nd > 3) reinterpret_cast<unsigned*>(dst + 3 * p.plane)[i] = __byte_perm(q01, q23, 0x7632);
+          const int4* __restrict__ src = reinterpret_cast<const int4*>(band + ((size_t)bs * 2 + x) * p.seg_alloc);
+          unsigned* __restrict__ d0 = reinterpret_cast<unsigned*>(stream + ((size_t)ss * 2 + x) * p.dmax * p.plane);
+          unsigned* __restrict__ d1 = d0 + p.plane / 4;
+          for (int i0 = tb; i0 < n4; i0 += 4 * kI8BuildThreads) {
+            int4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int i = i0 + k * kI8BuildThreads;
+              v[k] = i < n4 ? src[i] : make_int4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int i = i0 + k * kI8BuildThreads;
+              range |= ((unsigned)v[k].x + 32768u) | ((unsigned)v[k].y + 32768u) | ((unsigned)v[k].z + 32768u) |
+                       ((unsigned)v[k].w + 32768u);
+              const unsigned p01 = __byte_perm(v[k].x, v[k].y, 0x5140), p23 = __byte_perm(v[k].z, v[k].w, 0x5140);
+              if (i < n4) {
+                d0[i] = __byte_perm(p01, p23, 0x5410);
+                d1[i] = __byte_perm(p01, p23, 0x7632);
+              }
             }
           }
         }
         // every staged value in [-32768, 32767]: two digits suffice for this (row, term)
         const unsigned any_big = __any_sync(0xffffffffu, (range >> 16) != 0u);
         if (lane == 0) sflag[ss * 4 + (warp - kI8FirstBuild)] = any_big ? 0 : 1;
+        if (nd > 2) {
+          named_bar(3, kI8BuildThreads);
+          bool big = false;
+          for (int w = 0; w < kI8BuildWarps; ++w) big = big || sflag[ss * 4 + w] == 0;
+          // pass 2 (rare): the digit planes >= 2 for the MMA's three- or four-digit products
+          if (big)
+            for (int x = 0; x < 2; ++x) {
+              const int4* __restrict__ src = reinterpret_cast<const int4*>(band + ((size_t)bs * 2 + x) * p.seg_alloc);
+              unsigned* __restrict__ d2 = reinterpret_cast<unsigned*>(stream + ((size_t)ss * 2 + x) * p.dmax * p.plane) +
+                                          2 * (p.plane / 4);
+              for (int i = tb; i < n4; i += kI8BuildThreads) {
+                const int4 v = src[i];
+                const unsigned q01 = __byte_perm(v.x, v.y, 0x7362), q23 = __byte_perm(v.z, v.w, 0x7362);
+                d2[i] = __byte_perm(q01, q23, 0x5410);
+                if (nd > 3) d2[i + p.plane / 4] = __byte_perm(q01, q23, 0x7632);
+              }
+            }
+        }
         fence_proxy_async_smem();                   // digit planes -> visible to the tensor core
         mbar_arrive(&sfull[ss]);
         mbar_arrive(&bandempty[bs]);
@@ -304,11 +341,11 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     const int te = threadIdx.x - 32 * kI8FirstEpi;
     const int quarter = warp & 3, h = (warp - kI8FirstEpi) >> 2;
     const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
-    uint32_t q = 0;
+    uint32_t q = 0, nst = 0;
     int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
       unsigned sre[2][8], sim[2][8];                                    // running corr (mod 2^32), per tile
-      for (int step = 0; step < nterms; ++step, par ^= 1) {
+      for (int step = 0; step < nterms; ++step) {
         const int ti = p.J - step;
         PeakI best;
         best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
@@ -354,18 +391,38 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           mbar_arrive(&dempty[buf]);
           ++q;
           const int tau0 = 2048 * t + 16 * c + 8 * h;
-          if (tau0 < p.N) {
+          const bool valid = tau0 < p.N;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (step == 0) { sre[t][i] = re[i]; sim[t][i] = im[i]; }
-              else { sre[t][i] += re[i]; sim[t][i] += im[i]; }
-            }
-            if (p.want_corr) {
-              int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * p.N + tau0);
+          for (int i = 0; i < 8; ++i) {
+            if (step == 0) { sre[t][i] = re[i]; sim[t][i] = im[i]; }
+            else { sre[t][i] += re[i]; sim[t][i] += im[i]; }
+          }
+          if (p.want_corr && !p.tma_store && valid) {
+            int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * p.N + tau0);
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                dst[i] = make_int4((int)sre[t][2 * i], (int)sim[t][2 * i], (int)sre[t][2 * i + 1], (int)sim[t][2 * i + 1]);
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_int4((int)sre[t][2 * i], (int)sim[t][2 * i], (int)sre[t][2 * i + 1], (int)sim[t][2 * i + 1]);
+          }
+          if (p.want_corr && p.tma_store) {
+            // corr_ti of this warp's 32 lag blocks (8 lags each) -> 64B-swizzled staging -> one TMA
+            // tensor store (32 x 64 B); the staging buffer of two stores ago must have been read
+            unsigned char* sb = stg + ((size_t)(warp - kI8FirstEpi) * 2 + (nst & 1)) * kI8StgBytes;
+            if (lane == 0) bulk_wait_read_le1();
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              *reinterpret_cast<int4*>(sb + 64 * lane + 16 * (k ^ ((lane >> 1) & 3))) =
+                  make_int4((int)sre[t][2 * k], (int)sim[t][2 * k], (int)sre[t][2 * k + 1], (int)sim[t][2 * k + 1]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const long long blk = (((long long)row * nterms + ti) * p.N + 2048 * t + 16 * 32 * quarter) >> 4;
+              tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
+              bulk_commit();
             }
+            ++nst;
+          }
+          if (valid) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const unsigned long long m = mag2i((int)sre[t][i], (int)sim[t][i]);
@@ -375,29 +432,33 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
             }
           }
         }
-        // the row's peak at scale ti: warp argmax (high word, low word, smallest lag), then 8 warps
+        // the row's peak at scale ti: warp argmax (high word, low word, smallest lag) -> partial
         const bool ok = best.tau >= 0;
         const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
         const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
         const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
         const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
         const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
-        PeakI* rp = red + par * kI8EpiWarps;
+        PeakI* rp = red + ((size_t)par * kI8MaxTerms + ti) * kI8EpiWarps;
         if (ok && (unsigned)best.tau == tmin) rp[warp - kI8FirstEpi] = best;
         else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[warp - kI8FirstEpi] = e; }
-        named_bar(2, 32 * kI8EpiWarps);
-        if (te == 0 && lag) {
-          PeakI b = rp[0];
-          for (int w = 1; w < kI8EpiWarps; ++w) {
-            const PeakI o = rp[w];
-            if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
-          }
-          const size_t e = (size_t)row * nterms + ti;
-          lag[e] = b.tau;
-          if (val) val[e] = make_int2(b.re, b.im);
-        }
       }
+      // every scale of the row: combine the warps' partials (one barrier per row)
+      named_bar(2, 32 * kI8EpiWarps);
+      if (te < nterms && lag) {
+        const PeakI* rp = red + ((size_t)par * kI8MaxTerms + te) * kI8EpiWarps;
+        PeakI b = rp[0];
+        for (int w = 1; w < kI8EpiWarps; ++w) {
+          const PeakI o = rp[w];
+          if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
+        }
+        const size_t e = (size_t)row * nterms + te;
+        lag[e] = b.tau;
+        if (val) val[e] = make_int2(b.re, b.im);
+      }
+      par ^= 1;
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -521,8 +582,29 @@ cudaError_t i8_build_images(const I8Params& p, const int2* d_taps, const int* to
   return e;
 }
 
-cudaError_t i8_launch(const I8Params& p, const int* bands, const unsigned char* img, int2* corr, int32_t* lag,
+// corr [rows][J+1][N] int2 as a 3-D TMA tensor of 8-byte elements: [lag blocks of 16][2 halves][8 lags];
+// box = 8 lags x 1 half x 32 blocks (one epilogue warp's tile slice), 64-byte swizzle
+static bool encode_corr_map_i8(CUtensorMap* map, void* corr, long long rows, const I8Params& p) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  const cuuint64_t dims[3] = {8, 2, (cuuint64_t)rows * (p.J + 1) * (p.N / 16)};
+  const cuuint64_t strides[2] = {64, 128};
+  const cuuint32_t box[3] = {8, 1, 32};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, corr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t i8_launch(const I8Params& p0, const int* bands, const unsigned char* img, int2* corr, int32_t* lag,
                       int2* val, int grid, cudaStream_t s) {
+  I8Params p = p0;
+  p.tma_store = (p.N % 512 == 0) ? 1 : 0;
+  if (corr && p.tma_store && !encode_corr_map_i8(&p.cmap, corr, p.rows, p)) return cudaErrorInvalidValue;
   const size_t smem = i8_layout(p).total;
   void (*kern)(const int*, const unsigned char*, int2*, int32_t*, int2*, const I8Params);
   switch (p.tn) {

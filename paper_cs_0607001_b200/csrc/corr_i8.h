@@ -5,6 +5,7 @@
 // contraction is carried out on byte digits with int32 accumulation -- exact -- and the
 // digit products are recombined with shifts in the epilogue.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -27,10 +28,12 @@ struct I8Term {
 };
 
 struct I8Params {
+  CUtensorMap cmap;                   // corr as [rows (J+1) N / 16 lag blocks][2 halves][8 lags] of 8-byte elements
   int N, J, stride, ML, ntiles, tn, ncol, dmax;
   int nband, nstream, nimg;           // ring depths: staged band segments, digit streams, B images
   int seg_alloc, plane, img_alloc;    // int32 per component per band stage; bytes per digit plane; bytes per image stage
   int want_corr;
+  int tma_store;                      // corr_s written by TMA tensor stores (N a multiple of 512), else st.global
   long long rows;
   I8Term term[kI8MaxTerms];           // by processing step (0 = coarsest, a_J)
 };
