@@ -101,6 +101,31 @@ __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&r)[8]
 }
 __device__ __forceinline__ void tmem_wait_ld_all() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
+// the 8 TN accumulator columns of one (digit, component, half): x8 / x16 / x32 shapes
+template <int TN>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[8 * TN]) {
+  if constexpr (TN == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr) : "memory");
+  } else {
+#pragma unroll
+    for (int a = 0; a < TN; ++a) {
+      uint32_t* x = r + 8 * a;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                   : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+                   : "r"(taddr + 8 * a) : "memory");
+    }
+  }
+}
+template <int NR>
+__device__ __forceinline__ void tie_regs(uint32_t (&r)[NR]) {   // uses of r are ordered after the preceding wait
+#pragma unroll
+  for (int i = 0; i < NR; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 // 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread (no wait)
 __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
@@ -134,7 +159,7 @@ __global__ void k_i8_images(const int2* __restrict__ taps, I8Params p, const int
   const I8Term tm = p.term[step];
   const int ks = rest - base;
   const int ti = p.J - step;
-  const int oc = n / (16 * p.tn), a = (n / 16) % p.tn, pp = n % 16;
+  const int oc = n / (16 * p.tn), hh = (n / (8 * p.tn)) & 1, a = (n / 8) % p.tn, pp = 8 * hh + (n % 8);
   const int g = 1 << tm.lg;
   unsigned char* blk = img + tm.img_ofs + (size_t)(ks * 2 + x) * p.ncol * 32;
   for (int j = 0; j < 32; ++j) {
@@ -337,101 +362,114 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       }
   } else {
     // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
-    // Two warps per TMEM lane quarter; warp half h takes shifts p = 8h .. 8h+7 of every lag block.
+    // Two warps per TMEM lane quarter; warp half h takes shifts p = 8h .. 8h+7 of every lag block,
+    // i.e. accumulator columns oc (16 TN) + h (8 TN) + [0, 8 TN): digit a of shift 8h + pl at a 8 + pl.
     const int te = threadIdx.x - 32 * kI8FirstEpi;
     const int quarter = warp & 3, h = (warp - kI8FirstEpi) >> 2;
     const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
+    const int N = p.N, ntiles = p.ntiles;
+    const bool want_corr = p.want_corr != 0, tma = p.tma_store != 0;
+    unsigned char* sbase = stg + (size_t)(warp - kI8FirstEpi) * 2 * kI8StgBytes;
     uint32_t q = 0, nst = 0;
     int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      unsigned sre[2][8], sim[2][8];                                    // running corr (mod 2^32), per tile
+      unsigned sr0[8], si0[8], sr1[8], si1[8];                          // running corr (mod 2^32) of tiles 0, 1
       for (int step = 0; step < nterms; ++step) {
         const int ti = p.J - step;
         PeakI best;
         best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (t >= p.ntiles) break;
+        // one tile: D_ti (digits recombined mod 2^32) added into the running sums (sr, si)
+        auto tile = [&](int t, unsigned (&sr)[8], unsigned (&si)[8]) {
           const uint32_t buf = q % NBUF;
           mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
           const int D = dcnt[buf];
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + 8 * TN * h;
           unsigned re[8], im[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) { re[i] = 0u; im[i] = 0u; }
-          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + 8 * h;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            if (b >= D) break;
-            uint32_t v[2][TN][8];                                       // every load of digit b, one wait
-#pragma unroll
-            for (int oc = 0; oc < 2; ++oc)
-#pragma unroll
-              for (int a = 0; a < TN; ++a) tmem_ld8_nowait(tb0 + b * NCOL + oc * 16 * TN + 16 * a, v[oc][a]);
+          {
+            uint32_t v0[8 * TN], w0[8 * TN], v1[8 * TN], w1[8 * TN];     // digits 0 and 1 of (re, im)
+            tmem_ld_cols<TN>(tb0, v0);
+            tmem_ld_cols<TN>(tb0 + 16 * TN, w0);
+            tmem_ld_cols<TN>(tb0 + NCOL, v1);
+            tmem_ld_cols<TN>(tb0 + NCOL + 16 * TN, w1);
             tmem_wait_ld_all();
+            tie_regs(v0); tie_regs(w0); tie_regs(v1); tie_regs(w1);
 #pragma unroll
-            for (int oc = 0; oc < 2; ++oc)
-#pragma unroll
-              for (int a = 0; a < TN; ++a)
-#pragma unroll
-                for (int i = 0; i < 8; ++i) asm volatile("" : "+r"(v[oc][a][i]));   // uses after the wait
-#pragma unroll
-            for (int oc = 0; oc < 2; ++oc)
+            for (int i = 0; i < 8; ++i) {
+              unsigned r = v0[i], m = w0[i];
 #pragma unroll
               for (int a = 0; a < TN; ++a) {
-                const int sh = 8 * (a + b);
+                if (a > 0) { r += v0[8 * a + i] << (8 * a); m += w0[8 * a + i] << (8 * a); }
+                r += v1[8 * a + i] << (8 * a + 8);
+                m += w1[8 * a + i] << (8 * a + 8);
+              }
+              re[i] = r; im[i] = m;
+            }
+          }
+          for (int bq = 2; bq < D; ++bq) {                              // rare: third / fourth data digit
+            uint32_t v[8 * TN], w[8 * TN];
+            tmem_ld_cols<TN>(tb0 + bq * NCOL, v);
+            tmem_ld_cols<TN>(tb0 + bq * NCOL + 16 * TN, w);
+            tmem_wait_ld_all();
+            tie_regs(v); tie_regs(w);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  if (oc == 0) re[i] += v[oc][a][i] << sh;
-                  else im[i] += v[oc][a][i] << sh;
-                }
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+              for (int a = 0; a < TN; ++a) {
+                re[i] += v[8 * a + i] << (8 * (a + bq));
+                im[i] += w[8 * a + i] << (8 * (a + bq));
               }
           }
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
           ++q;
           const int tau0 = 2048 * t + 16 * c + 8 * h;
-          const bool valid = tau0 < p.N;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (step == 0) { sre[t][i] = re[i]; sim[t][i] = im[i]; }
-            else { sre[t][i] += re[i]; sim[t][i] += im[i]; }
+            if (step == 0) { sr[i] = re[i]; si[i] = im[i]; }
+            else { sr[i] += re[i]; si[i] += im[i]; }
           }
-          if (p.want_corr && !p.tma_store && valid) {
-            int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * p.N + tau0);
+          if (want_corr && !tma && tau0 < N) {
+            int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tau0);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              dst[i] = make_int4((int)sre[t][2 * i], (int)sim[t][2 * i], (int)sre[t][2 * i + 1], (int)sim[t][2 * i + 1]);
+              dst[i] = make_int4((int)sr[2 * i], (int)si[2 * i], (int)sr[2 * i + 1], (int)si[2 * i + 1]);
           }
-          if (p.want_corr && p.tma_store) {
+          if (want_corr && tma) {
             // corr_ti of this warp's 32 lag blocks (8 lags each) -> 64B-swizzled staging -> one TMA
             // tensor store (32 x 64 B); the staging buffer of two stores ago must have been read
-            unsigned char* sb = stg + ((size_t)(warp - kI8FirstEpi) * 2 + (nst & 1)) * kI8StgBytes;
+            unsigned char* sb = sbase + (nst & 1) * kI8StgBytes;
             if (lane == 0) bulk_wait_read_le1();
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               *reinterpret_cast<int4*>(sb + 64 * lane + 16 * (k ^ ((lane >> 1) & 3))) =
-                  make_int4((int)sre[t][2 * k], (int)sim[t][2 * k], (int)sre[t][2 * k + 1], (int)sim[t][2 * k + 1]);
+                  make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) {
-              const long long blk = (((long long)row * nterms + ti) * p.N + 2048 * t + 16 * 32 * quarter) >> 4;
+            if (lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's 32 blocks all in or all out
+              const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
               tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
               bulk_commit();
             }
             ++nst;
           }
-          if (valid) {
+          if (tau0 < N) {
+            // peak candidates in lag order: strict '>' keeps the smallest lag of a tie
+            if (best.tau < 0) { best.m2 = mag2i((int)sr[0], (int)si[0]); best.tau = tau0; best.re = (int)sr[0]; best.im = (int)si[0]; }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const unsigned long long m = mag2i((int)sre[t][i], (int)sim[t][i]);
-              if (best.tau < 0 || m > best.m2) {
-                best.m2 = m; best.tau = tau0 + i; best.re = (int)sre[t][i]; best.im = (int)sim[t][i];
-              }
+              const unsigned long long m = mag2i((int)sr[i], (int)si[i]);
+              const bool gt = m > best.m2;
+              best.m2 = gt ? m : best.m2;
+              best.tau = gt ? tau0 + i : best.tau;
+              best.re = gt ? (int)sr[i] : best.re;
+              best.im = gt ? (int)si[i] : best.im;
             }
           }
-        }
+        };
+        tile(0, sr0, si0);
+        if (ntiles > 1) tile(1, sr1, si1);
         // the row's peak at scale ti: warp argmax (high word, low word, smallest lag) -> partial
         const bool ok = best.tau >= 0;
         const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
