@@ -34,9 +34,10 @@
 // HBM (128 contiguous bytes per thread) and the row's peak per scale (a7) is reduced in the
 // epilogue -- no partials, no finalize kernel.
 //
-// Roles (320 threads): warp 0 bulk-copy loader (band segments of both components, B images);
-// warp 1 MMA issuer; warps 2-5 builders (int32 band segment -> byte-digit planes, range
-// flag); warps 6-9 epilogue (TMEM lane quarter = warp % 4).
+// Roles (704 threads): warp 0 bulk-copy loader (band segments of both components, B images);
+// warp 1 MMA issuer (whole warp, one elected lane issues); warps 2-5 builders (int32 band segment
+// -> byte-digit planes, range flag); warps 6-21 epilogue, four per TMEM lane quarter (warp % 4),
+// each four of the 16 shifts of a lag block; corr leaves through swizzled staging and TMA stores.
 #define SIDWT_NO_KERNELS
 #include "kernels.cuh"
 #include "corr_tc.cuh"
@@ -49,7 +50,9 @@
 
 namespace sidwt {
 
-constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6, kI8EpiWarps = 8;
+// epilogue: kI8HW warps per TMEM lane quarter, each kI8PL of the 16 shifts of every lag block
+constexpr int kI8HW = 4, kI8PL = 16 / kI8HW;
+constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6, kI8EpiWarps = 4 * kI8HW;
 constexpr int kI8Warps = kI8FirstEpi + kI8EpiWarps;
 constexpr int kI8Threads = 32 * kI8Warps;
 constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
@@ -58,11 +61,12 @@ constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
 constexpr int kI8TmemCols = 512;
 
 struct I8Smem { size_t red, stg, band, stream, img, total; };
-constexpr int kI8StgBytes = 2048;                   // per epilogue warp and buffer: 32 lag blocks x 8 lags x 8 B
+constexpr int kI8RowBytes = 8 * kI8PL;             // one lane's corr slice: kI8PL lags x 8 B (32, 64 or 128: TMA swizzle span)
+constexpr int kI8StgBytes = 32 * kI8RowBytes;       // per epilogue warp and buffer: 32 lag blocks
 __host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
   I8Smem L;
   L.red = 1024;                                                         // [2 rows][J+1][kI8EpiWarps] peak partials
-  L.stg = (L.red + (size_t)2 * kI8MaxTerms * kI8EpiWarps * 24 + 1023) & ~(size_t)1023;   // 64B-swizzled TMA staging
+  L.stg = (L.red + (size_t)2 * kI8MaxTerms * kI8EpiWarps * 24 + 1023) & ~(size_t)1023;   // swizzled TMA staging
   L.band = L.stg + (size_t)kI8EpiWarps * 2 * kI8StgBytes;
   L.stream = (L.band + (size_t)p.nband * 2 * p.seg_alloc * 4 + 127) & ~(size_t)127;
   L.img = L.stream + (size_t)p.nstream * 2 * p.dmax * p.plane;
@@ -101,23 +105,20 @@ __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t (&r)[8]
 }
 __device__ __forceinline__ void tmem_wait_ld_all() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
-// the 8 TN accumulator columns of one (digit, component, half): x8 / x16 / x32 shapes
-template <int TN>
-__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[8 * TN]) {
-  if constexpr (TN == 2) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                 : "r"(taddr) : "memory");
-  } else {
+// NC consecutive accumulator columns (NC a multiple of 4): x8 pieces, then an x4 tail
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) {
 #pragma unroll
-    for (int a = 0; a < TN; ++a) {
-      uint32_t* x = r + 8 * a;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                   : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
-                   : "r"(taddr + 8 * a) : "memory");
-    }
+  for (int o = 0; o + 8 <= NC; o += 8) {
+    uint32_t* x = r + o;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+                 : "r"(taddr + o) : "memory");
+  }
+  if constexpr (NC % 8 == 4) {
+    uint32_t* x = r + NC - 4;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(taddr + NC - 4) : "memory");
   }
 }
 template <int NR>
@@ -159,7 +160,8 @@ __global__ void k_i8_images(const int2* __restrict__ taps, I8Params p, const int
   const I8Term tm = p.term[step];
   const int ks = rest - base;
   const int ti = p.J - step;
-  const int oc = n / (16 * p.tn), hh = (n / (8 * p.tn)) & 1, a = (n / 8) % p.tn, pp = 8 * hh + (n % 8);
+  const int oc = n / (16 * p.tn), hh = (n / (kI8PL * p.tn)) % kI8HW, a = (n / kI8PL) % p.tn;
+  const int pp = kI8PL * hh + (n % kI8PL);
   const int g = 1 << tm.lg;
   unsigned char* blk = img + tm.img_ofs + (size_t)(ks * 2 + x) * p.ncol * 32;
   for (int j = 0; j < 32; ++j) {
@@ -362,8 +364,9 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       }
   } else {
     // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
-    // Two warps per TMEM lane quarter; warp half h takes shifts p = 8h .. 8h+7 of every lag block,
-    // i.e. accumulator columns oc (16 TN) + h (8 TN) + [0, 8 TN): digit a of shift 8h + pl at a 8 + pl.
+    // kI8HW warps per TMEM lane quarter; warp h of a quarter takes shifts p = PL h .. PL h + PL-1
+    // of every lag block, i.e. accumulator columns oc (16 TN) + h (PL TN) + a PL + pl.
+    constexpr int PL = kI8PL, NC = kI8PL * TN;
     const int te = threadIdx.x - 32 * kI8FirstEpi;
     const int quarter = warp & 3, h = (warp - kI8FirstEpi) >> 2;
     const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
@@ -373,77 +376,80 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     uint32_t q = 0, nst = 0;
     int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      unsigned sr0[8], si0[8], sr1[8], si1[8];                          // running corr (mod 2^32) of tiles 0, 1
+      unsigned sr0[PL], si0[PL], sr1[PL], si1[PL];                      // running corr (mod 2^32) of tiles 0, 1
       for (int step = 0; step < nterms; ++step) {
         const int ti = p.J - step;
         PeakI best;
         best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
         // one tile: D_ti (digits recombined mod 2^32) added into the running sums (sr, si)
-        auto tile = [&](int t, unsigned (&sr)[8], unsigned (&si)[8]) {
+        auto tile = [&](int t, unsigned (&sr)[PL], unsigned (&si)[PL]) {
           const uint32_t buf = q % NBUF;
           mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
           const int D = dcnt[buf];
-          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + 8 * TN * h;
-          unsigned re[8], im[8];
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + NC * h;
+          unsigned re[PL], im[PL];
           {
-            uint32_t v0[8 * TN], w0[8 * TN], v1[8 * TN], w1[8 * TN];     // digits 0 and 1 of (re, im)
-            tmem_ld_cols<TN>(tb0, v0);
-            tmem_ld_cols<TN>(tb0 + 16 * TN, w0);
-            tmem_ld_cols<TN>(tb0 + NCOL, v1);
-            tmem_ld_cols<TN>(tb0 + NCOL + 16 * TN, w1);
+            uint32_t v0[NC], w0[NC], v1[NC], w1[NC];                     // digits 0 and 1 of (re, im)
+            tmem_ld_cols<NC>(tb0, v0);
+            tmem_ld_cols<NC>(tb0 + 16 * TN, w0);
+            tmem_ld_cols<NC>(tb0 + NCOL, v1);
+            tmem_ld_cols<NC>(tb0 + NCOL + 16 * TN, w1);
             tmem_wait_ld_all();
             tie_regs(v0); tie_regs(w0); tie_regs(v1); tie_regs(w1);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < PL; ++i) {
               unsigned r = v0[i], m = w0[i];
 #pragma unroll
               for (int a = 0; a < TN; ++a) {
-                if (a > 0) { r += v0[8 * a + i] << (8 * a); m += w0[8 * a + i] << (8 * a); }
-                r += v1[8 * a + i] << (8 * a + 8);
-                m += w1[8 * a + i] << (8 * a + 8);
+                if (a > 0) { r += v0[PL * a + i] << (8 * a); m += w0[PL * a + i] << (8 * a); }
+                r += v1[PL * a + i] << (8 * a + 8);
+                m += w1[PL * a + i] << (8 * a + 8);
               }
               re[i] = r; im[i] = m;
             }
           }
           for (int bq = 2; bq < D; ++bq) {                              // rare: third / fourth data digit
-            uint32_t v[8 * TN], w[8 * TN];
-            tmem_ld_cols<TN>(tb0 + bq * NCOL, v);
-            tmem_ld_cols<TN>(tb0 + bq * NCOL + 16 * TN, w);
+            uint32_t v[NC], w[NC];
+            tmem_ld_cols<NC>(tb0 + bq * NCOL, v);
+            tmem_ld_cols<NC>(tb0 + bq * NCOL + 16 * TN, w);
             tmem_wait_ld_all();
             tie_regs(v); tie_regs(w);
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < PL; ++i)
 #pragma unroll
               for (int a = 0; a < TN; ++a) {
-                re[i] += v[8 * a + i] << (8 * (a + bq));
-                im[i] += w[8 * a + i] << (8 * (a + bq));
+                re[i] += v[PL * a + i] << (8 * (a + bq));
+                im[i] += w[PL * a + i] << (8 * (a + bq));
               }
           }
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
           ++q;
-          const int tau0 = 2048 * t + 16 * c + 8 * h;
+          const int tau0 = 2048 * t + 16 * c + PL * h;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < PL; ++i) {
             if (step == 0) { sr[i] = re[i]; si[i] = im[i]; }
             else { sr[i] += re[i]; si[i] += im[i]; }
           }
           if (want_corr && !tma && tau0 < N) {
             int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tau0);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < PL / 2; ++i)
               dst[i] = make_int4((int)sr[2 * i], (int)si[2 * i], (int)sr[2 * i + 1], (int)si[2 * i + 1]);
           }
           if (want_corr && tma) {
-            // corr_ti of this warp's 32 lag blocks (8 lags each) -> 64B-swizzled staging -> one TMA
-            // tensor store (32 x 64 B); the staging buffer of two stores ago must have been read
+            // corr_ti of this warp's 32 lag blocks (PL lags each) -> swizzled staging (the TMA map's
+            // swizzle span = one lane's row) -> one TMA tensor store; the staging buffer of two
+            // stores ago must have been read
             unsigned char* sb = sbase + (nst & 1) * kI8StgBytes;
             if (lane == 0) bulk_wait_read_le1();
             __syncwarp();
+            constexpr int CH = kI8RowBytes / 16;                        // 16-byte chunks per row
+            const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              *reinterpret_cast<int4*>(sb + 64 * lane + 16 * (k ^ ((lane >> 1) & 3))) =
+            for (int k = 0; k < CH; ++k)
+              *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (k ^ sw)) =
                   make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
             fence_proxy_async_smem();
             __syncwarp();
@@ -458,7 +464,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
             // peak candidates in lag order: strict '>' keeps the smallest lag of a tie
             if (best.tau < 0) { best.m2 = mag2i((int)sr[0], (int)si[0]); best.tau = tau0; best.re = (int)sr[0]; best.im = (int)si[0]; }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < PL; ++i) {
               const unsigned long long m = mag2i((int)sr[i], (int)si[i]);
               const bool gt = m > best.m2;
               best.m2 = gt ? m : best.m2;
@@ -587,13 +593,14 @@ bool i8_configure(I8Params& p, int N, int J, int stride, int ML, const int* kmin
   int img_alloc = 0;
   for (int step = 0; step <= J; ++step) img_alloc = std::max(img_alloc, p.term[step].ksteps * 2 * p.ncol * 32);
   p.img_alloc = (img_alloc + 127) & ~127;
-  p.nstream = 2;
-  p.nimg = 2;
+  // ring depths: as many staged band segments as fit (>= 2), two digit-stream stages (one for
+  // deep plans whose planes are long, e.g. J = 10), two B-image stages
   const size_t budget = 227 * 1024;
-  for (p.nband = 4; p.nband >= 2; --p.nband)
-    if (i8_layout(p).total <= budget) break;
-  if (i8_layout(p).total > budget) return false;
-  return true;
+  p.nimg = 2;
+  for (p.nstream = 2; p.nstream >= 1; --p.nstream)
+    for (p.nband = 4; p.nband >= 2; --p.nband)
+      if (i8_layout(p).total <= budget) return true;
+  return false;
 }
 
 size_t i8_image_bytes(const I8Params& p) {
@@ -620,8 +627,8 @@ cudaError_t i8_build_images(const I8Params& p, const int2* d_taps, const int* to
   return e;
 }
 
-// corr [rows][J+1][N] int2 as a 3-D TMA tensor of 8-byte elements: [lag blocks of 16][2 halves][8 lags];
-// box = 8 lags x 1 half x 32 blocks (one epilogue warp's tile slice), 64-byte swizzle
+// corr [rows][J+1][N] int2 as a 3-D TMA tensor of 8-byte elements: [lag blocks of 16][kI8HW parts][kI8PL
+// lags]; box = kI8PL lags x 1 part x 32 blocks (one epilogue warp's tile slice), swizzle span = one row
 static bool encode_corr_map_i8(CUtensorMap* map, void* corr, long long rows, const I8Params& p) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
@@ -630,12 +637,14 @@ static bool encode_corr_map_i8(CUtensorMap* map, void* corr, long long rows, con
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return false;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }
-  const cuuint64_t dims[3] = {8, 2, (cuuint64_t)rows * (p.J + 1) * (p.N / 16)};
-  const cuuint64_t strides[2] = {64, 128};
-  const cuuint32_t box[3] = {8, 1, 32};
+  const cuuint64_t dims[3] = {kI8PL, kI8HW, (cuuint64_t)rows * (p.J + 1) * (p.N / 16)};
+  const cuuint64_t strides[2] = {kI8RowBytes, 128};
+  const cuuint32_t box[3] = {kI8PL, 1, 32};
+  const CUtensorMapSwizzle sw = kI8RowBytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                : (kI8RowBytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, corr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t i8_launch(const I8Params& p0, const int* bands, const unsigned char* img, int2* corr, int32_t* lag,
