@@ -26,7 +26,9 @@
 //       16-byte windows of taps 2ks and 2ks+1 -- and B is diagonal (j mod 16 = p).
 //   conj(t) w = (tr wr + ti wi) + i (tr wi - ti wr): the wr stream meets B columns
 //   (re: tr, im: -ti), the wi stream (re: ti, im: tr); both accumulate into the same TMEM.
-//   One accumulator per data digit b: [128 lanes][ncol] int32; TMEM double-buffered by tile.
+//   Data digit b's MMAs write at TMEM column offset 32 b, so the products of equal weight
+//   256^(a+b) land in the same 32-column group: the tensor core forms the digit groups
+//   c = a + b itself (D + Tn - 1 groups of [128 lanes][32] int32), TMEM double-buffered by tile.
 //
 // Eq. (4): one CTA owns a whole row (persistent over rows), terms coarsest
 // first; every epilogue thread owns the same 16 lags of each 2048-lag tile for all terms, so
@@ -34,10 +36,10 @@
 // HBM (128 contiguous bytes per thread) and the row's peak per scale (a7) is reduced in the
 // epilogue -- no partials, no finalize kernel.
 //
-// Roles (704 threads): warp 0 bulk-copy loader (band segments of both components, B images);
+// Roles (448 threads): warp 0 bulk-copy loader (band segments of both components, B images);
 // warp 1 MMA issuer (whole warp, one elected lane issues); warps 2-5 builders (int32 band segment
-// -> byte-digit planes, range flag); warps 6-21 epilogue, four per TMEM lane quarter (warp % 4),
-// each four of the 16 shifts of a lag block; corr leaves through swizzled staging and TMA stores.
+// -> byte-digit planes, range flag); warps 6-13 epilogue, two per TMEM lane quarter (warp % 4),
+// each eight of the 16 shifts of a lag block; corr leaves through swizzled staging and TMA stores.
 #define SIDWT_NO_KERNELS
 #include "kernels.cuh"
 #include "corr_tc.cuh"
@@ -51,7 +53,8 @@
 namespace sidwt {
 
 // epilogue: kI8HW warps per TMEM lane quarter, each kI8PL of the 16 shifts of every lag block
-constexpr int kI8HW = 4, kI8PL = 16 / kI8HW;
+constexpr int kI8HW = 2, kI8PL = 16 / kI8HW;     // measured: 4 warps per quarter issue-bound (C5 corr 9.05 vs 8.38 ms)
+static_assert(kI8HW == 2, "accumulator column order n = 32 a + 16 (p / 8) + 8 oc + p % 8 assumes two halves");
 constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6, kI8EpiWarps = 4 * kI8HW;
 constexpr int kI8Warps = kI8FirstEpi + kI8EpiWarps;
 constexpr int kI8Threads = 32 * kI8Warps;
@@ -145,8 +148,8 @@ __device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
 
 // B operand images: for each processing step, K step ks, data component x (0: wr, 1: wi), an
 // [ncol][32 bytes] K-major no-swizzle block, element (n, j) at (n/8)*256 + (j/16)*128 + (n%8)*16
-// + j%16; column n = oc (16 tn) + 16 a + p holds digit a of the coefficient that multiplies the
-// x stream for output component oc at shift p.  One thread per (step, ks, x, n).
+// + j%16; column n = 32 a + 16 (p / 8) + 8 oc + p % 8 holds digit a of the coefficient that multiplies
+// the x stream for output component oc at shift p.  One thread per (step, ks, x, n).
 __global__ void k_i8_images(const int2* __restrict__ taps, I8Params p, const int* toff_by_term, int total,
                             unsigned char* __restrict__ img) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -160,8 +163,7 @@ __global__ void k_i8_images(const int2* __restrict__ taps, I8Params p, const int
   const I8Term tm = p.term[step];
   const int ks = rest - base;
   const int ti = p.J - step;
-  const int oc = n / (16 * p.tn), hh = (n / (kI8PL * p.tn)) % kI8HW, a = (n / kI8PL) % p.tn;
-  const int pp = kI8PL * hh + (n % kI8PL);
+  const int a = n / 32, oc = (n / 8) & 1, pp = 8 * ((n / 16) & 1) + (n % 8);
   const int g = 1 << tm.lg;
   unsigned char* blk = img + tm.img_ofs + (size_t)(ks * 2 + x) * p.ncol * 32;
   for (int j = 0; j < 32; ++j) {
@@ -221,7 +223,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tslot, kI8TmemCols);
-  const int NBUF = p.dmax * NCOL <= kI8TmemCols / 2 ? 2 : 1;
+  // accumulator span: digit-weight groups c = a + b = 0 .. dmax + TN - 2, 32 columns each
+  const int NBUF = (p.dmax + TN - 1) * 32 <= kI8TmemCols / 2 ? 2 : 1;
   const uint32_t bufcols = kI8TmemCols / NBUF;
   tc_fence_before();
   __syncthreads();
@@ -279,15 +282,27 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           __syncwarp();
           const uint32_t dt = tmem + buf * bufcols;
           if (elect_one()) {
+            // data digit b's products land at columns 32 b + n: the digit-weight groups c = a + b
+            // (32 columns each, weight 256^c) are summed by the tensor core itself.  At the first K
+            // step, the group a new digit reaches first (c = b + TN - 1) starts fresh.
             for (int x = 0; x < 2; ++x)
               for (int ks = 0; ks < ksteps; ++ks) {
                 const uint64_t bd = bdesc0 + (uint64_t)((ks * 2 + x) * (NCOL * 2));
                 const uint64_t ad = adesc0 + (uint64_t)(x * p.dmax * plane16 + 128 * t + ks * kadv16);
-                const uint32_t acc = (x | ks) ? 1u : 0u;
-                umma_i8(dt, ad, bd, id0, acc);
-                if (D > 1) umma_i8(dt + NCOL, ad + plane16, bd, id1, acc);
-                if (D > 2) umma_i8(dt + 2 * NCOL, ad + 2 * plane16, bd, id2, acc);
-                if (D > 3) umma_i8(dt + 3 * NCOL, ad + 3 * plane16, bd, id3, acc);
+                const bool first = (x | ks) == 0;
+                umma_i8(dt, ad, bd, id0, first ? 0u : 1u);
+#pragma unroll
+                for (int b = 1; b < 4; ++b) {
+                  if (b >= D) break;
+                  const uint32_t idb = b == 1 ? id1 : (b == 2 ? id2 : id3);
+                  if (first && TN > 1) {
+                    umma_i8(dt + 32 * b, ad + b * plane16, bd, (idb & ~(0x3Fu << 17)) | ((uint32_t)(32 * (TN - 1) >> 3) << 17), 1u);
+                    umma_i8(dt + 32 * (b + TN - 1), ad + b * plane16, bd + (uint64_t)(64 * (TN - 1)),
+                            (idb & ~(0x3Fu << 17)) | (4u << 17), 0u);
+                  } else {
+                    umma_i8(dt + 32 * b, ad + b * plane16, bd, idb, first ? 0u : 1u);
+                  }
+                }
               }
             umma_commit(&dfull[buf]);
           }
@@ -387,41 +402,32 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
           const int D = dcnt[buf];
-          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + NC * h;
+          // group c at columns 32 c + 16 h + [oc 8 + pl]: one x16 load per group
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + 16 * h;
           unsigned re[PL], im[PL];
           {
-            uint32_t v0[NC], w0[NC], v1[NC], w1[NC];                     // digits 0 and 1 of (re, im)
-            tmem_ld_cols<NC>(tb0, v0);
-            tmem_ld_cols<NC>(tb0 + 16 * TN, w0);
-            tmem_ld_cols<NC>(tb0 + NCOL, v1);
-            tmem_ld_cols<NC>(tb0 + NCOL + 16 * TN, w1);
+            // groups 0, 1 always exist (D >= 2), group 2 whenever TN >= 2
+            uint32_t g0[16], g1[16], g2[16];
+            tmem_ld_cols<16>(tb0, g0);
+            tmem_ld_cols<16>(tb0 + 32, g1);
+            if constexpr (TN >= 2) tmem_ld_cols<16>(tb0 + 64, g2);
             tmem_wait_ld_all();
-            tie_regs(v0); tie_regs(w0); tie_regs(v1); tie_regs(w1);
+            tie_regs(g0); tie_regs(g1);
+            if constexpr (TN >= 2) tie_regs(g2);
 #pragma unroll
             for (int i = 0; i < PL; ++i) {
-              unsigned r = v0[i], m = w0[i];
-#pragma unroll
-              for (int a = 0; a < TN; ++a) {
-                if (a > 0) { r += v0[PL * a + i] << (8 * a); m += w0[PL * a + i] << (8 * a); }
-                r += v1[PL * a + i] << (8 * a + 8);
-                m += w1[PL * a + i] << (8 * a + 8);
-              }
-              re[i] = r; im[i] = m;
+              re[i] = g0[i] + (g1[i] << 8);
+              im[i] = g0[8 + i] + (g1[8 + i] << 8);
+              if constexpr (TN >= 2) { re[i] += g2[i] << 16; im[i] += g2[8 + i] << 16; }
             }
           }
-          for (int bq = 2; bq < D; ++bq) {                              // rare: third / fourth data digit
-            uint32_t v[NC], w[NC];
-            tmem_ld_cols<NC>(tb0 + bq * NCOL, v);
-            tmem_ld_cols<NC>(tb0 + bq * NCOL + 16 * TN, w);
+          for (int cq = TN >= 2 ? 3 : 2; cq < D + TN - 1; ++cq) {      // rare: higher digit-weight groups
+            uint32_t g[16];
+            tmem_ld_cols<16>(tb0 + 32 * cq, g);
             tmem_wait_ld_all();
-            tie_regs(v); tie_regs(w);
+            tie_regs(g);
 #pragma unroll
-            for (int i = 0; i < PL; ++i)
-#pragma unroll
-              for (int a = 0; a < TN; ++a) {
-                re[i] += v[PL * a + i] << (8 * (a + bq));
-                im[i] += w[PL * a + i] << (8 * (a + bq));
-              }
+            for (int i = 0; i < PL; ++i) { re[i] += g[i] << (8 * cq); im[i] += g[8 + i] << (8 * cq); }
           }
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
@@ -587,7 +593,7 @@ bool i8_configure(I8Params& p, int N, int J, int stride, int ML, const int* kmin
     img += tm.ksteps * 2 * p.ncol * 32;
   }
   p.dmax = dmax;
-  if (dmax * p.ncol > kI8TmemCols) return false;
+  if ((dmax + tn - 1) * 32 > kI8TmemCols) return false;
   p.seg_alloc = (seg_alloc + 3) & ~3;
   p.plane = (int)((std::max(2048 * p.ntiles - 16 + kwin, seg_alloc) + 127) & ~127);
   int img_alloc = 0;
@@ -596,10 +602,10 @@ bool i8_configure(I8Params& p, int N, int J, int stride, int ML, const int* kmin
   // ring depths: as many staged band segments as fit (>= 2), two digit-stream stages (one for
   // deep plans whose planes are long, e.g. J = 10), two B-image stages
   const size_t budget = 227 * 1024;
-  p.nimg = 2;
-  for (p.nstream = 2; p.nstream >= 1; --p.nstream)
-    for (p.nband = 4; p.nband >= 2; --p.nband)
-      if (i8_layout(p).total <= budget) return true;
+  for (p.nimg = 2; p.nimg >= 1; --p.nimg)
+    for (p.nstream = 2; p.nstream >= 1; --p.nstream)
+      for (p.nband = 4; p.nband >= 2; --p.nband)
+        if (i8_layout(p).total <= budget) return true;
   return false;
 }
 
