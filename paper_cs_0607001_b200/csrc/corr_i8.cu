@@ -56,7 +56,8 @@ namespace sidwt {
 constexpr int kI8HW = 2, kI8PL = 16 / kI8HW;     // measured: 4 warps per quarter issue-bound (C5 corr 9.05 vs 8.38 ms)
 static_assert(kI8HW == 2, "accumulator column order n = 32 a + 16 (p / 8) + 8 oc + p % 8 assumes two halves");
 constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6, kI8EpiWarps = 4 * kI8HW;
-constexpr int kI8Warps = kI8FirstEpi + kI8EpiWarps;
+constexpr int kI8Mma2 = kI8FirstEpi + kI8EpiWarps;      // second MMA-issuing warp
+constexpr int kI8Warps = kI8Mma2 + 1;
 constexpr int kI8Threads = 32 * kI8Warps;
 constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
 // TMEM: 512 columns, two accumulator buffers of 256 (tile t+1's MMAs overlap tile t's epilogue)
@@ -188,6 +189,36 @@ __global__ void k_i8_images(const int2* __restrict__ taps, I8Params p, const int
   }
 }
 
+// The MMAs of one 2048-lag tile: for data component x and K step ks, data digit b's products go
+// to TMEM column offset 32 b (equal-weight digit products sum in the same 32-column group); at
+// the first K step the group a digit reaches first (c = b + TN - 1) starts fresh.  A signedness:
+// the top digit signed, the others unsigned.  D (digits in use) is a template parameter so the
+// issue sequence is straight-line.
+template <int TN, int D>
+__device__ __forceinline__ void i8_issue_tile(uint32_t dt, uint64_t a_t, uint64_t bdesc0, uint32_t idesc0, int ksteps,
+                                              int kadv16, uint32_t xstride16, uint32_t plane16) {
+  constexpr uint32_t kNsplit = ((uint32_t)(32 * (TN > 1 ? TN - 1 : 1)) >> 3) << 17;
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    uint64_t ad = a_t + (uint64_t)(x * xstride16);
+    uint64_t bd = bdesc0 + (uint64_t)(x * 64 * TN);
+    for (int ks = 0; ks < ksteps; ++ks, ad += (uint64_t)kadv16, bd += (uint64_t)(128 * TN)) {
+      const bool first = (x | ks) == 0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        const uint32_t idb = idesc0 | (b == D - 1 ? (1u << 7) : 0u);
+        if (b > 0 && TN > 1 && first) {
+          umma_i8(dt + 32 * b, ad + b * plane16, bd, (idb & ~(0x3Fu << 17)) | kNsplit, 1u);
+          umma_i8(dt + 32 * (b + TN - 1), ad + b * plane16, bd + (uint64_t)(64 * (TN - 1)),
+                  (idb & ~(0x3Fu << 17)) | (4u << 17), 0u);
+        } else {
+          umma_i8(dt + 32 * b, ad + b * plane16, bd, idb, first ? 0u : 1u);
+        }
+      }
+    }
+  }
+}
+
 template <int TN>
 __global__ void __launch_bounds__(kI8Threads, 1)
 k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ img, int2* __restrict__ corr,
@@ -215,17 +246,19 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   const int nterms = p.J + 1;
   constexpr int NCOL = 32 * TN;
 
+  // accumulator span: digit-weight groups c = a + b = 0 .. dmax + TN - 2, 32 columns each
+  const int NBUF = (p.dmax + TN - 1) * 32 <= kI8TmemCols / 2 ? 2 : 1;
+  const uint32_t bufcols = kI8TmemCols / NBUF;
+  // two MMA-issuing warps (one tile each) when a row has two tiles and TMEM is double-buffered
+  const int nmma = (p.ntiles >= 2 && NBUF == 2) ? 2 : 1;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) { mbar_init(&bandfull[i], 1); mbar_init(&bandempty[i], kI8BuildThreads); }
-    for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], 1); }
-    for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], 1); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], nmma); }
+    for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], nmma); }
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * kI8EpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tslot, kI8TmemCols);
-  // accumulator span: digit-weight groups c = a + b = 0 .. dmax + TN - 2, 32 columns each
-  const int NBUF = (p.dmax + TN - 1) * 32 <= kI8TmemCols / 2 ? 2 : 1;
-  const uint32_t bufcols = kI8TmemCols / NBUF;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -252,9 +285,11 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           bulk_load_g2s(imgs + (size_t)is * p.img_alloc, img + tm.img_ofs, ib, &imgfull[is]);
         }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer: the whole warp runs the loop (uniform values stay in uniform
-    // registers), one elected lane issues the MMAs and their commits
+  } else if (warp == 1 || warp == kI8Mma2) {
+    // ---------------- MMA issuers: two warps, warp k issues the MMAs of tiles t = k (mod 2) (one
+    // tile per warp for N = 4096), so the two tiles' issue latencies overlap.  The whole warp runs
+    // the loop (uniform values in uniform registers); one elected lane issues MMAs and commits.
+    const int mw = warp == 1 ? 0 : 1;
     const uint32_t idesc0 = (2u << 4) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t st0 = smem_u32(stream), im0 = smem_u32(imgs);
     const uint32_t plane16 = (uint32_t)p.plane >> 4;
@@ -263,18 +298,17 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       for (int step = 0; step < nterms; ++step, ++u) {
         const int ksteps = p.term[step].ksteps, kadv16 = p.term[step].kadv >> 4, dig = p.term[step].dig;
         const uint32_t ss = u % NS, is = u % NI;
+        if (mw >= nmma) continue;                                          // single issuer: the second warp idles
         mbar_wait(&sfull[ss], (u / NS) & 1);
         mbar_wait(&imgfull[is], (u / NI) & 1);
         tc_fence_after();
         bool fits = true;
         for (int w = 0; w < kI8BuildWarps; ++w) fits = fits && sflag[ss * 4 + w] != 0;
         const int D = (fits && dig > 2) ? 2 : dig;
-        // A signedness: the top digit signed, the others unsigned
-        const uint32_t id0 = idesc0 | (D == 1 ? (1u << 7) : 0u), id1 = idesc0 | (D == 2 ? (1u << 7) : 0u);
-        const uint32_t id2 = idesc0 | (D == 3 ? (1u << 7) : 0u), id3 = idesc0 | (1u << 7);
         const uint64_t bdesc0 = smem_desc(im0 + is * p.img_alloc, 128, 256);
         const uint64_t adesc0 = smem_desc(st0 + ss * 2 * p.dmax * p.plane, (uint32_t)p.term[step].lbo, 128);
         for (int t = 0; t < p.ntiles; ++t, ++q) {
+          if (t % nmma != mw) continue;
           const uint32_t buf = q % NBUF;
           mbar_wait(&dempty[buf], ((q / NBUF) & 1) ^ 1);
           tc_fence_after();
@@ -282,28 +316,12 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           __syncwarp();
           const uint32_t dt = tmem + buf * bufcols;
           if (elect_one()) {
-            // data digit b's products land at columns 32 b + n: the digit-weight groups c = a + b
-            // (32 columns each, weight 256^c) are summed by the tensor core itself.  At the first K
-            // step, the group a new digit reaches first (c = b + TN - 1) starts fresh.
-            for (int x = 0; x < 2; ++x)
-              for (int ks = 0; ks < ksteps; ++ks) {
-                const uint64_t bd = bdesc0 + (uint64_t)((ks * 2 + x) * (NCOL * 2));
-                const uint64_t ad = adesc0 + (uint64_t)(x * p.dmax * plane16 + 128 * t + ks * kadv16);
-                const bool first = (x | ks) == 0;
-                umma_i8(dt, ad, bd, id0, first ? 0u : 1u);
-#pragma unroll
-                for (int b = 1; b < 4; ++b) {
-                  if (b >= D) break;
-                  const uint32_t idb = b == 1 ? id1 : (b == 2 ? id2 : id3);
-                  if (first && TN > 1) {
-                    umma_i8(dt + 32 * b, ad + b * plane16, bd, (idb & ~(0x3Fu << 17)) | ((uint32_t)(32 * (TN - 1) >> 3) << 17), 1u);
-                    umma_i8(dt + 32 * (b + TN - 1), ad + b * plane16, bd + (uint64_t)(64 * (TN - 1)),
-                            (idb & ~(0x3Fu << 17)) | (4u << 17), 0u);
-                  } else {
-                    umma_i8(dt + 32 * b, ad + b * plane16, bd, idb, first ? 0u : 1u);
-                  }
-                }
-              }
+            const uint64_t a_t = adesc0 + (uint64_t)(128 * t);
+            switch (D) {
+              case 2: i8_issue_tile<TN, 2>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
+              case 3: i8_issue_tile<TN, 3>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
+              default: i8_issue_tile<TN, 4>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
+            }
             umma_commit(&dfull[buf]);
           }
           __syncwarp();
@@ -377,7 +395,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         mbar_arrive(&sfull[ss]);
         mbar_arrive(&bandempty[bs]);
       }
-  } else {
+  } else if (warp < kI8FirstEpi + kI8EpiWarps) {
     // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
     // kI8HW warps per TMEM lane quarter; warp h of a quarter takes shifts p = PL h .. PL h + PL-1
     // of every lag block, i.e. accumulator columns oc (16 TN) + h (PL TN) + a PL + pl.
