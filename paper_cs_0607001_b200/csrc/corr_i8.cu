@@ -495,27 +495,43 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           tmem_ld_cols<16>(tb0 + 32, g1);
           if constexpr (TN >= 2) tmem_ld_cols<16>(tb0 + 64, g2);
         }
+        // unit k's groups leave TMEM first (the MMA waits on this buffer for the next term), then
+        // unit k-1 is finished, then unit k's digits are recombined
+        uint32_t g3[16];
+        bool more = false;
+        if (have) {
+          tmem_wait_ld_all();
+          tie_regs(g0); tie_regs(g1);
+          if constexpr (TN >= 2) tie_regs(g2);
+          more = G > (TN >= 2 ? 3 : 2);
+          if (more) {                                                     // rare: a fourth group (three-digit term)
+            tmem_ld_cols<16>(tb0 + 32 * (TN >= 2 ? 3 : 2), g3);
+            tmem_wait_ld_all();
+            tie_regs(g3);
+          }
+          for (int cq = TN >= 2 ? 4 : 3; cq < G; ++cq) {                  // rarer still: more groups
+            uint32_t g[16];
+            tmem_ld_cols<16>(tb0 + 32 * cq, g);
+            tmem_wait_ld_all();
+            tie_regs(g);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) g3[i] += g[i] << (8 * (cq - (TN >= 2 ? 3 : 2)));
+          }
+          tc_fence_before();
+          mbar_arrive(&dempty[t]);
+        }
         if (k > 0) finish(k - 1);
         if (!have) break;
-        tmem_wait_ld_all();
-        tie_regs(g0); tie_regs(g1);
-        if constexpr (TN >= 2) tie_regs(g2);
 #pragma unroll
         for (int i = 0; i < PL; ++i) {
           pre[i] = g0[i] + (g1[i] << 8);
           pim[i] = g0[8 + i] + (g1[8 + i] << 8);
           if constexpr (TN >= 2) { pre[i] += g2[i] << 16; pim[i] += g2[8 + i] << 16; }
+          if (more) {
+            constexpr int s3 = TN >= 2 ? 24 : 16;
+            pre[i] += g3[i] << s3; pim[i] += g3[8 + i] << s3;
+          }
         }
-        for (int cq = TN >= 2 ? 3 : 2; cq < G; ++cq) {                 // rare: higher digit-weight groups
-          uint32_t g[16];
-          tmem_ld_cols<16>(tb0 + 32 * cq, g);
-          tmem_wait_ld_all();
-          tie_regs(g);
-#pragma unroll
-          for (int i = 0; i < PL; ++i) { pre[i] += g[i] << (8 * cq); pim[i] += g[8 + i] << (8 * cq); }
-        }
-        tc_fence_before();
-        mbar_arrive(&dempty[t]);
         const int tau0 = 2048 * t + 16 * c + PL * h;
         if (want_corr && !tma && tau0 < N) {
           int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tau0);
