@@ -60,18 +60,17 @@ constexpr int kI8Mma2 = kI8FirstEpi + kI8EpiWarps;      // second MMA-issuing wa
 constexpr int kI8Warps = kI8Mma2 + 1;
 constexpr int kI8Threads = 32 * kI8Warps;
 constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
-// TMEM: 512 columns, one 256-column accumulator per 2048-lag tile (two tiles: N <= 4096), kept
-// for a row's terms (eq. (4) accumulates in TMEM)
-constexpr int kI8TmemCols = 512, kI8BufCols = 256;
+// TMEM: 512 columns, two accumulator buffers of 256 (tile t+1's MMAs overlap tile t's epilogue)
+// when dmax * ncol <= 256, else one buffer of 512
+constexpr int kI8TmemCols = 512;
 
-struct I8Smem { size_t red, zero, stg, band, stream, img, total; };
+struct I8Smem { size_t red, stg, band, stream, img, total; };
 constexpr int kI8RowBytes = 8 * kI8PL;             // one lane's corr slice: kI8PL lags x 8 B (32, 64 or 128: TMA swizzle span)
 constexpr int kI8StgBytes = 32 * kI8RowBytes;       // per epilogue warp and buffer: 32 lag blocks
 __host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
   I8Smem L;
   L.red = 1024;                                                         // [2 rows][J+1][kI8EpiWarps] peak partials
-  L.zero = (L.red + (size_t)2 * kI8MaxTerms * kI8EpiWarps * 24 + 127) & ~(size_t)127;    // 32 x 32 B zero B block
-  L.stg = (L.zero + 1024 + 1023) & ~(size_t)1023;                                        // swizzled TMA staging
+  L.stg = (L.red + (size_t)2 * kI8MaxTerms * kI8EpiWarps * 24 + 1023) & ~(size_t)1023;   // swizzled TMA staging
   L.band = L.stg + (size_t)kI8EpiWarps * 2 * kI8StgBytes;
   L.stream = (L.band + (size_t)p.nband * 2 * p.seg_alloc * 4 + 127) & ~(size_t)127;
   L.img = L.stream + (size_t)p.nstream * 2 * p.dmax * p.plane;
@@ -190,14 +189,12 @@ __global__ void k_i8_images(const int2* __restrict__ taps, I8Params p, const int
   }
 }
 
-// The MMAs of one 2048-lag tile for one term: for data component x and K step ks, data digit
-// b's products go to TMEM column offset 32 b, so equal-weight digit products (weight 256^(a+b))
-// sum in the same 32-column group.  Eq. (4): the accumulator persists over a row's terms (coarsest
-// first), so after term i it holds corr_i; only the row's first term (FRESH) starts it, at its
-// first K step (the group a new digit reaches first, c = b + TN - 1, starts fresh).  A
-// signedness: the top digit signed, the others unsigned.  D (digits in use) is a template
-// parameter so the issue sequence is straight-line.
-template <int TN, int D, bool FRESH>
+// The MMAs of one 2048-lag tile: for data component x and K step ks, data digit b's products go
+// to TMEM column offset 32 b (equal-weight digit products sum in the same 32-column group); at
+// the first K step the group a digit reaches first (c = b + TN - 1) starts fresh.  A signedness:
+// the top digit signed, the others unsigned.  D (digits in use) is a template parameter so the
+// issue sequence is straight-line.
+template <int TN, int D>
 __device__ __forceinline__ void i8_issue_tile(uint32_t dt, uint64_t a_t, uint64_t bdesc0, uint32_t idesc0, int ksteps,
                                               int kadv16, uint32_t xstride16, uint32_t plane16) {
   constexpr uint32_t kNsplit = ((uint32_t)(32 * (TN > 1 ? TN - 1 : 1)) >> 3) << 17;
@@ -206,7 +203,7 @@ __device__ __forceinline__ void i8_issue_tile(uint32_t dt, uint64_t a_t, uint64_
     uint64_t ad = a_t + (uint64_t)(x * xstride16);
     uint64_t bd = bdesc0 + (uint64_t)(x * 64 * TN);
     for (int ks = 0; ks < ksteps; ++ks, ad += (uint64_t)kadv16, bd += (uint64_t)(128 * TN)) {
-      const bool first = FRESH && (x | ks) == 0;
+      const bool first = (x | ks) == 0;
 #pragma unroll
       for (int b = 0; b < D; ++b) {
         const uint32_t idb = idesc0 | (b == D - 1 ? (1u << 7) : 0u);
@@ -242,7 +239,6 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   int* sflag = reinterpret_cast<int*>(smem_raw + 288);                // [4 stages][4 builder warps]
   PeakI* red = reinterpret_cast<PeakI*>(smem_raw + L.red);            // [2][kI8MaxTerms][kI8EpiWarps]
   unsigned char* stg = smem_raw + L.stg;                              // [kI8EpiWarps][2][kI8StgBytes]
-  unsigned char* zeroB = smem_raw + L.zero;
   int* band = reinterpret_cast<int*>(smem_raw + L.band);
   unsigned char* stream = smem_raw + L.stream;
   unsigned char* imgs = smem_raw + L.img;
@@ -250,10 +246,11 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   const int nterms = p.J + 1;
   constexpr int NCOL = 32 * TN;
 
-  // two MMA-issuing warps (one tile each) when a row has two tiles
-  const int nmma = p.ntiles >= 2 ? 2 : 1;
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<uint32_t*>(zeroB)[i] = 0u;
-  fence_proxy_async_smem();
+  // accumulator span: digit-weight groups c = a + b = 0 .. dmax + TN - 2, 32 columns each
+  const int NBUF = (p.dmax + TN - 1) * 32 <= kI8TmemCols / 2 ? 2 : 1;
+  const uint32_t bufcols = kI8TmemCols / NBUF;
+  // two MMA-issuing warps (one tile each) when a row has two tiles and TMEM is double-buffered
+  const int nmma = (p.ntiles >= 2 && NBUF == 2) ? 2 : 1;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) { mbar_init(&bandfull[i], 1); mbar_init(&bandempty[i], kI8BuildThreads); }
     for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], nmma); }
@@ -296,9 +293,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     const uint32_t idesc0 = (2u << 4) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t st0 = smem_u32(stream), im0 = smem_u32(imgs);
     const uint32_t plane16 = (uint32_t)p.plane >> 4;
-    const uint64_t zdesc = smem_desc(smem_u32(zeroB), 128, 256);
-    uint32_t u = 0;
-    int grow = 0;
+    uint32_t u = 0, q = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
       for (int step = 0; step < nterms; ++step, ++u) {
         const int ksteps = p.term[step].ksteps, kadv16 = p.term[step].kadv >> 4, dig = p.term[step].dig;
@@ -312,39 +307,22 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         const int D = (fits && dig > 2) ? 2 : dig;
         const uint64_t bdesc0 = smem_desc(im0 + is * p.img_alloc, 128, 256);
         const uint64_t adesc0 = smem_desc(st0 + ss * 2 * p.dmax * p.plane, (uint32_t)p.term[step].lbo, 128);
-        // the row's accumulator groups so far: [0, dmax + TN - 1) are defined from its first term
-        // (groups its digits do not reach are zeroed), the epilogue reads [0, G) with G the
-        // largest D + TN - 1 of the row's terms so far
-        if (step == 0) grow = 0;
-        grow = max(grow, D + TN - 1);
-        for (int t = 0; t < p.ntiles; ++t) {
+        for (int t = 0; t < p.ntiles; ++t, ++q) {
           if (t % nmma != mw) continue;
-          // TMEM buffer t holds tile t's accumulator for the whole row; the epilogue has read the
-          // previous term's values before this term accumulates on them
-          mbar_wait(&dempty[t], (u & 1) ^ 1);
+          const uint32_t buf = q % NBUF;
+          mbar_wait(&dempty[buf], ((q / NBUF) & 1) ^ 1);
           tc_fence_after();
-          if (lane == 0) dcnt[t] = grow;
+          if (lane == 0) dcnt[buf] = D;
           __syncwarp();
-          const uint32_t dt = tmem + t * kI8BufCols;
+          const uint32_t dt = tmem + buf * bufcols;
           if (elect_one()) {
             const uint64_t a_t = adesc0 + (uint64_t)(128 * t);
-            if (step == 0) {
-              switch (D) {
-                case 2: i8_issue_tile<TN, 2, true>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
-                case 3: i8_issue_tile<TN, 3, true>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
-                default: i8_issue_tile<TN, 4, true>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
-              }
-              // zero the groups this term's digits do not reach (a zero B block, accumulate off)
-              for (int cz = D + TN - 1; cz < p.dmax + TN - 1; ++cz)
-                umma_i8(dt + 32 * cz, a_t, zdesc, (idesc0 & ~(0x3Fu << 17)) | (4u << 17), 0u);
-            } else {
-              switch (D) {
-                case 2: i8_issue_tile<TN, 2, false>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
-                case 3: i8_issue_tile<TN, 3, false>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
-                default: i8_issue_tile<TN, 4, false>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
-              }
+            switch (D) {
+              case 2: i8_issue_tile<TN, 2>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
+              case 3: i8_issue_tile<TN, 3>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
+              default: i8_issue_tile<TN, 4>(dt, a_t, bdesc0, idesc0, ksteps, kadv16, p.dmax * plane16, plane16); break;
             }
-            umma_commit(&dfull[t]);
+            umma_commit(&dfull[buf]);
           }
           __syncwarp();
         }
@@ -418,142 +396,121 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         mbar_arrive(&bandempty[bs]);
       }
   } else if (warp < kI8FirstEpi + kI8EpiWarps) {
-    // ---------------- epilogue: TMEM (corr_i in digit-weight groups, eq. (4) accumulated by the
-    // tensor core) -> recombined mod 2^32 -> swizzled staging -> TMA store; peak per scale.
-    // Two warps per TMEM lane quarter; warp half h takes shifts p = 8h .. 8h+7 of every lag block:
-    // group c at columns 32 c + 16 h + [oc 8 + pl].
-    constexpr int PL = kI8PL;
+    // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
+    // kI8HW warps per TMEM lane quarter; warp h of a quarter takes shifts p = PL h .. PL h + PL-1
+    // of every lag block, i.e. accumulator columns oc (16 TN) + h (PL TN) + a PL + pl.
+    constexpr int PL = kI8PL, NC = kI8PL * TN;
     const int te = threadIdx.x - 32 * kI8FirstEpi;
     const int quarter = warp & 3, h = (warp - kI8FirstEpi) >> 2;
     const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
     const int N = p.N, ntiles = p.ntiles;
     const bool want_corr = p.want_corr != 0, tma = p.tma_store != 0;
     unsigned char* sbase = stg + (size_t)(warp - kI8FirstEpi) * 2 * kI8StgBytes;
-    uint32_t uterm = 0;                                                 // terms processed (TMEM buffer phase)
+    uint32_t q = 0, nst = 0;
     int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      PeakI best;
-      unsigned pre[PL], pim[PL];                                        // corr of the pending unit
-      // Units k = (term step, tile t) of the row, software-pipelined by one: iteration k issues
-      // the TMEM loads of unit k, then finishes unit k-1 (peak candidates, proxy fence, TMA
-      // store, the term's warp argmax after its last tile) while those loads are in flight,
-      // then recombines unit k's digit groups and stages its corr.
-      auto finish = [&](int k) {
-        const int step = k / ntiles, t = k - step * ntiles, ti = p.J - step;
-        const int tau0 = 2048 * t + 16 * c + PL * h;
-        if (t == 0) { best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0; }
-        if (tau0 < N) {
-          // peak candidates in lag order: strict '>' keeps the smallest lag of a tie
-          if (best.tau < 0) { best.m2 = mag2i((int)pre[0], (int)pim[0]); best.tau = tau0; best.re = (int)pre[0]; best.im = (int)pim[0]; }
-#pragma unroll
-          for (int i = 0; i < PL; ++i) {
-            const unsigned long long m = mag2i((int)pre[i], (int)pim[i]);
-            const bool gt = m > best.m2;
-            best.m2 = gt ? m : best.m2;
-            best.tau = gt ? tau0 + i : best.tau;
-            best.re = gt ? (int)pre[i] : best.re;
-            best.im = gt ? (int)pim[i] : best.im;
-          }
-        }
-        if (want_corr && tma) {
-          fence_proxy_async_smem();                                       // staging writes -> async proxy
-          __syncwarp();
-          if (lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's 32 blocks all in or all out
-            const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
-            tma_store_3d(&p.cmap, smem_u32(sbase + (k & 1) * kI8StgBytes), 0, h, (int)blk);
-            bulk_commit();
-          }
-        }
-        if (t == ntiles - 1) {
-          // the row's peak at scale ti: warp argmax (high word, low word, smallest lag) -> partial
-          const bool ok = best.tau >= 0;
-          const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
-          const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-          const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
-          const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
-          const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
-          PeakI* rp = red + ((size_t)par * kI8MaxTerms + ti) * kI8EpiWarps;
-          if (ok && (unsigned)best.tau == tmin) rp[warp - kI8FirstEpi] = best;
-          else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[warp - kI8FirstEpi] = e; }
-        }
-      };
-      const int nk = nterms * ntiles;
-      for (int k = 0; k <= nk; ++k) {
-        const bool have = k < nk;
-        const int step = k / ntiles, t = k - step * ntiles, ti = p.J - step;
-        uint32_t g0[16], g1[16], g2[16];
-        uint32_t tb0 = 0;
-        int G = 2;
-        const uint32_t ph = (uterm + step) & 1;
-        if (have) {
-          mbar_wait(&dfull[t], ph);
+      unsigned sr0[PL], si0[PL], sr1[PL], si1[PL];                      // running corr (mod 2^32) of tiles 0, 1
+      for (int step = 0; step < nterms; ++step) {
+        const int ti = p.J - step;
+        PeakI best;
+        best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
+        // one tile: D_ti (digits recombined mod 2^32) added into the running sums (sr, si)
+        auto tile = [&](int t, unsigned (&sr)[PL], unsigned (&si)[PL]) {
+          const uint32_t buf = q % NBUF;
+          mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
-          G = dcnt[t];
-          // groups 0, 1 always exist (D >= 2), group 2 whenever TN >= 2
-          tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + t * kI8BufCols + 16 * h;
-          tmem_ld_cols<16>(tb0, g0);
-          tmem_ld_cols<16>(tb0 + 32, g1);
-          if constexpr (TN >= 2) tmem_ld_cols<16>(tb0 + 64, g2);
-        }
-        // unit k's groups leave TMEM first (the MMA waits on this buffer for the next term), then
-        // unit k-1 is finished, then unit k's digits are recombined
-        uint32_t g3[16];
-        bool more = false;
-        if (have) {
-          tmem_wait_ld_all();
-          tie_regs(g0); tie_regs(g1);
-          if constexpr (TN >= 2) tie_regs(g2);
-          more = G > (TN >= 2 ? 3 : 2);
-          if (more) {                                                     // rare: a fourth group (three-digit term)
-            tmem_ld_cols<16>(tb0 + 32 * (TN >= 2 ? 3 : 2), g3);
+          const int D = dcnt[buf];
+          // group c at columns 32 c + 16 h + [oc 8 + pl]: one x16 load per group
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + 16 * h;
+          unsigned re[PL], im[PL];
+          {
+            // groups 0, 1 always exist (D >= 2), group 2 whenever TN >= 2
+            uint32_t g0[16], g1[16], g2[16];
+            tmem_ld_cols<16>(tb0, g0);
+            tmem_ld_cols<16>(tb0 + 32, g1);
+            if constexpr (TN >= 2) tmem_ld_cols<16>(tb0 + 64, g2);
             tmem_wait_ld_all();
-            tie_regs(g3);
+            tie_regs(g0); tie_regs(g1);
+            if constexpr (TN >= 2) tie_regs(g2);
+#pragma unroll
+            for (int i = 0; i < PL; ++i) {
+              re[i] = g0[i] + (g1[i] << 8);
+              im[i] = g0[8 + i] + (g1[8 + i] << 8);
+              if constexpr (TN >= 2) { re[i] += g2[i] << 16; im[i] += g2[8 + i] << 16; }
+            }
           }
-          for (int cq = TN >= 2 ? 4 : 3; cq < G; ++cq) {                  // rarer still: more groups
+          for (int cq = TN >= 2 ? 3 : 2; cq < D + TN - 1; ++cq) {      // rare: higher digit-weight groups
             uint32_t g[16];
             tmem_ld_cols<16>(tb0 + 32 * cq, g);
             tmem_wait_ld_all();
             tie_regs(g);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) g3[i] += g[i] << (8 * (cq - (TN >= 2 ? 3 : 2)));
+            for (int i = 0; i < PL; ++i) { re[i] += g[i] << (8 * cq); im[i] += g[8 + i] << (8 * cq); }
           }
           tc_fence_before();
-          mbar_arrive(&dempty[t]);
-        }
-        if (k > 0) finish(k - 1);
-        if (!have) break;
+          mbar_arrive(&dempty[buf]);
+          ++q;
+          const int tau0 = 2048 * t + 16 * c + PL * h;
 #pragma unroll
-        for (int i = 0; i < PL; ++i) {
-          pre[i] = g0[i] + (g1[i] << 8);
-          pim[i] = g0[8 + i] + (g1[8 + i] << 8);
-          if constexpr (TN >= 2) { pre[i] += g2[i] << 16; pim[i] += g2[8 + i] << 16; }
-          if (more) {
-            constexpr int s3 = TN >= 2 ? 24 : 16;
-            pre[i] += g3[i] << s3; pim[i] += g3[8 + i] << s3;
+          for (int i = 0; i < PL; ++i) {
+            if (step == 0) { sr[i] = re[i]; si[i] = im[i]; }
+            else { sr[i] += re[i]; si[i] += im[i]; }
           }
-        }
-        const int tau0 = 2048 * t + 16 * c + PL * h;
-        if (want_corr && !tma && tau0 < N) {
-          int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tau0);
+          if (want_corr && !tma && tau0 < N) {
+            int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tau0);
 #pragma unroll
-          for (int i = 0; i < PL / 2; ++i)
-            dst[i] = make_int4((int)pre[2 * i], (int)pim[2 * i], (int)pre[2 * i + 1], (int)pim[2 * i + 1]);
-        }
-        if (want_corr && tma) {
-          // corr_ti of this warp's 32 lag blocks -> swizzled staging (the TMA map's swizzle span =
-          // one lane's row); the buffer's store of two units ago must have been read
-          unsigned char* sb = sbase + (k & 1) * kI8StgBytes;
-          if (lane == 0) bulk_wait_read_le1();
-          __syncwarp();
-          constexpr int CH = kI8RowBytes / 16;                          // 16-byte chunks per row
-          const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
+            for (int i = 0; i < PL / 2; ++i)
+              dst[i] = make_int4((int)sr[2 * i], (int)si[2 * i], (int)sr[2 * i + 1], (int)si[2 * i + 1]);
+          }
+          if (want_corr && tma) {
+            // corr_ti of this warp's 32 lag blocks (PL lags each) -> swizzled staging (the TMA map's
+            // swizzle span = one lane's row) -> one TMA tensor store; the staging buffer of two
+            // stores ago must have been read
+            unsigned char* sb = sbase + (nst & 1) * kI8StgBytes;
+            if (lane == 0) bulk_wait_read_le1();
+            __syncwarp();
+            constexpr int CH = kI8RowBytes / 16;                        // 16-byte chunks per row
+            const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
 #pragma unroll
-          for (int kk = 0; kk < CH; ++kk)
-            *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (kk ^ sw)) =
-                make_int4((int)pre[2 * kk], (int)pim[2 * kk], (int)pre[2 * kk + 1], (int)pim[2 * kk + 1]);
-        }
+            for (int k = 0; k < CH; ++k)
+              *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (k ^ sw)) =
+                  make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's 32 blocks all in or all out
+              const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
+              tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
+              bulk_commit();
+            }
+            ++nst;
+          }
+          if (tau0 < N) {
+            // peak candidates in lag order: strict '>' keeps the smallest lag of a tie
+            if (best.tau < 0) { best.m2 = mag2i((int)sr[0], (int)si[0]); best.tau = tau0; best.re = (int)sr[0]; best.im = (int)si[0]; }
+#pragma unroll
+            for (int i = 0; i < PL; ++i) {
+              const unsigned long long m = mag2i((int)sr[i], (int)si[i]);
+              const bool gt = m > best.m2;
+              best.m2 = gt ? m : best.m2;
+              best.tau = gt ? tau0 + i : best.tau;
+              best.re = gt ? (int)sr[i] : best.re;
+              best.im = gt ? (int)si[i] : best.im;
+            }
+          }
+        };
+        tile(0, sr0, si0);
+        if (ntiles > 1) tile(1, sr1, si1);
+        // the row's peak at scale ti: warp argmax (high word, low word, smallest lag) -> partial
+        const bool ok = best.tau >= 0;
+        const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
+        const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
+        const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
+        PeakI* rp = red + ((size_t)par * kI8MaxTerms + ti) * kI8EpiWarps;
+        if (ok && (unsigned)best.tau == tmin) rp[warp - kI8FirstEpi] = best;
+        else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[warp - kI8FirstEpi] = e; }
       }
-      uterm += nterms;
       // every scale of the row: combine the warps' partials (one barrier per row)
       named_bar(2, 32 * kI8EpiWarps);
       if (te < nterms && lag) {
@@ -654,7 +611,7 @@ bool i8_configure(I8Params& p, int N, int J, int stride, int ML, const int* kmin
     img += tm.ksteps * 2 * p.ncol * 32;
   }
   p.dmax = dmax;
-  if ((dmax + tn - 1) * 32 > kI8BufCols) return false;
+  if ((dmax + tn - 1) * 32 > kI8TmemCols) return false;
   p.seg_alloc = (seg_alloc + 3) & ~3;
   p.plane = (int)((std::max(2048 * p.ntiles - 16 + kwin, seg_alloc) + 127) & ~127);
   int img_alloc = 0;
