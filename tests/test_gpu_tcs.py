@@ -113,7 +113,8 @@ def test_tcs_exact_cdf97():
 
 
 def test_tcs_not_taken():
-    """Periodic extension, banks, the integer family and short rows stay on the SIMT kernel."""
+    """Periodic extension, banks and short rows stay on the SIMT kernel; the integer family takes
+    its own int8 tensor-core kernel (tests/test_gpu_i8.py), never this one."""
     rng = np.random.default_rng(5)
     one = (rng.normal(size=(1, 40)) + 1j * rng.normal(size=(1, 40))).astype(np.complex64)
     assert _plan(1, 3, 4096, 1, 0, one).tensor_core_path() == 0                    # periodic
@@ -122,4 +123,4 @@ def test_tcs_not_taken():
     assert _plan(1, 7, 4096, 1, 1, one).tensor_core_path() == 0                    # 2^J > N / 64
     assert _plan(1, 3, 4096, 1, 1, np.repeat(one, 2, 0)).tensor_core_path() == 0  # two templates
     it = rng.integers(-100, 100, size=(1, 40, 2)).astype(np.int16)
-    assert _plan(3, 3, 4096, 1, 1, it).tensor_core_path() == 0                     # integer
+    assert _plan(3, 3, 4096, 1, 1, it).tensor_core_path() == 3                     # integer: int8 kernel
