@@ -48,6 +48,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace sidwt {
@@ -267,6 +268,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  long long pw[3] = {0, 0, 0};                                        // -DSIDWT_TC_PROFILE: wait cycles per role
+  const long long p_t0 = TC_CLOCK();
 
   if (warp == 0) {
     // ---------------- loader: band segments (both components) and the term's B images
@@ -276,14 +279,14 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         for (int step = 0; step < nterms; ++step, ++u) {
           const I8Term& tm = p.term[step];
           const uint32_t bs = u % NB, is = u % NI;
-          mbar_wait(&bandempty[bs], ((u / NB) & 1) ^ 1);
+          TC_TWAIT(&bandempty[bs], ((u / NB) & 1) ^ 1, pw[0]);
           const uint32_t bytes = (uint32_t)tm.seg_len * 4u;
           mbar_expect_tx(&bandfull[bs], 2 * bytes);
           const int* src = bands + ((size_t)row * nterms + tm.band) * 2 * p.stride + tm.seg_a4;
           int* dst = band + (size_t)bs * 2 * p.seg_alloc;
           bulk_load_g2s(dst, src, bytes, &bandfull[bs]);
           bulk_load_g2s(dst + p.seg_alloc, src + p.stride, bytes, &bandfull[bs]);
-          mbar_wait(&imgempty[is], ((u / NI) & 1) ^ 1);
+          TC_TWAIT(&imgempty[is], ((u / NI) & 1) ^ 1, pw[1]);
           const uint32_t ib = (uint32_t)tm.ksteps * 2 * NCOL * 32;
           mbar_expect_tx(&imgfull[is], ib);
           bulk_load_g2s(imgs + (size_t)is * p.img_alloc, img + tm.img_ofs, ib, &imgfull[is]);
@@ -303,8 +306,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         const int ksteps = p.term[step].ksteps, kadv16 = p.term[step].kadv >> 4, dig = p.term[step].dig;
         const uint32_t ss = u % NS, is = u % NI;
         if (mw >= nmma) continue;                                          // single issuer: the second warp idles
-        mbar_wait(&sfull[ss], (u / NS) & 1);
-        mbar_wait(&imgfull[is], (u / NI) & 1);
+        TC_TWAIT(&sfull[ss], (u / NS) & 1, pw[0]);
+        TC_TWAIT(&imgfull[is], (u / NI) & 1, pw[1]);
         tc_fence_after();
         bool fits = true;
         for (int w = 0; w < kI8BuildWarps; ++w) fits = fits && sflag[ss * 4 + w] != 0;
@@ -314,7 +317,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         for (int t = 0; t < p.ntiles; ++t, ++q) {
           if (t % nmma != mw) continue;
           const uint32_t buf = q % NBUF;
-          mbar_wait(&dempty[buf], ((q / NBUF) & 1) ^ 1);
+          TC_TWAIT(&dempty[buf], ((q / NBUF) & 1) ^ 1, pw[2]);
           tc_fence_after();
           if (lane == 0) dcnt[buf] = D;
           __syncwarp();
@@ -344,8 +347,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       for (int step = 0; step < nterms; ++step, ++u) {
         const I8Term& tm = p.term[step];
         const uint32_t bs = u % NB, ss = u % NS;
-        mbar_wait(&bandfull[bs], (u / NB) & 1);
-        mbar_wait(&sempty[ss], ((u / NS) & 1) ^ 1);
+        TC_TWAIT(&bandfull[bs], (u / NB) & 1, pw[0]);
+        TC_TWAIT(&sempty[ss], ((u / NS) & 1) ^ 1, pw[1]);
         const int nd = tm.dig;
         const int n4 = tm.seg_len >> 2;
         unsigned range = 0;
@@ -420,7 +423,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         // one tile: D_ti (digits recombined mod 2^32) added into the running sums (sr, si)
         auto tile = [&](int t, unsigned (&sr)[PL], unsigned (&si)[PL]) {
           const uint32_t buf = q % NBUF;
-          mbar_wait(&dfull[buf], (q / NBUF) & 1);
+          TC_TWAIT(&dfull[buf], (q / NBUF) & 1, pw[0]);
           tc_fence_after();
           const int D = dcnt[buf];
           // group c at columns 32 c + 16 h + [oc 8 + pl]: one x16 load per group
@@ -470,7 +473,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           const int b = nst & 1;
           unsigned char* sb = sbase + b * kI8StgBytes;
           if (lane == 0) bulk_wait_read_le1();
-          mbar_wait(&stgempty[2 * e + b], ((nst >> 1) & 1) ^ 1);
+          TC_TWAIT(&stgempty[2 * e + b], ((nst >> 1) & 1) ^ 1, pw[1]);
           __syncwarp();
           constexpr int CH = kI8RowBytes / 16;                          // 16-byte chunks per row
           const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
@@ -516,11 +519,11 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           const int b = nst & 1;
           const uint32_t ph = (nst >> 1) & 1;
           int4 v[2 * CH];
-          mbar_wait(&stgfull[2 * e0 + b], ph);
+          TC_TWAIT(&stgfull[2 * e0 + b], ph, pw[0]);
 #pragma unroll
           for (int kk = 0; kk < CH; ++kk)
             v[kk] = *reinterpret_cast<const int4*>(sb0 + b * kI8StgBytes + kI8RowBytes * lane + 16 * (kk ^ sw));
-          mbar_wait(&stgfull[2 * e1 + b], ph);
+          TC_TWAIT(&stgfull[2 * e1 + b], ph, pw[1]);
 #pragma unroll
           for (int kk = 0; kk < CH; ++kk)
             v[CH + kk] = *reinterpret_cast<const int4*>(sb1 + b * kI8StgBytes + kI8RowBytes * lane + 16 * (kk ^ sw));
@@ -569,6 +572,10 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       par ^= 1;
     }
   }
+#ifdef SIDWT_TC_PROFILE
+  if (p.prof && blockIdx.x == 0 && lane == 0 && (warp <= 2 || warp == kI8FirstEpi || warp == kI8Mma2 || warp == kI8FirstPeak))
+    printf("i8 cta0 warp %2d: total %lld wait %lld %lld %lld\n", warp, TC_CLOCK() - p_t0, pw[0], pw[1], pw[2]);
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, kI8TmemCols);
@@ -716,6 +723,7 @@ cudaError_t i8_launch(const I8Params& p0, const int* bands, const unsigned char*
                       int2* val, int grid, cudaStream_t s) {
   I8Params p = p0;
   p.tma_store = (p.N % 512 == 0) ? 1 : 0;
+  if (const char* ev = std::getenv("SIDWT_TC_PROF")) p.prof = atoi(ev);
   if (corr && p.tma_store && !encode_corr_map_i8(&p.cmap, corr, p.rows, p)) return cudaErrorInvalidValue;
   const size_t smem = i8_layout(p).total;
   void (*kern)(const int*, const unsigned char*, int2*, int32_t*, int2*, const I8Params);
