@@ -268,7 +268,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  long long pw[3] = {0, 0, 0};                                        // -DSIDWT_TC_PROFILE: wait cycles per role
+  long long pw[4] = {0, 0, 0, 0};                                     // -DSIDWT_TC_PROFILE: wait / phase cycles per role
   const long long p_t0 = TC_CLOCK();
 
   if (warp == 0) {
@@ -424,6 +424,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         auto tile = [&](int t, unsigned (&sr)[PL], unsigned (&si)[PL]) {
           const uint32_t buf = q % NBUF;
           TC_TWAIT(&dfull[buf], (q / NBUF) & 1, pw[0]);
+          const long long p_a = TC_CLOCK();
           tc_fence_after();
           const int D = dcnt[buf];
           // group c at columns 32 c + 16 h + [oc 8 + pl]: one x16 load per group
@@ -456,6 +457,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
           ++q;
+          const long long p_b = TC_CLOCK();
+          pw[2] += p_b - p_a;
           const int tau0 = 2048 * t + 16 * c + PL * h;
 #pragma unroll
           for (int i = 0; i < PL; ++i) {
@@ -489,6 +492,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
             tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
             bulk_commit();
           }
+          pw[3] += TC_CLOCK() - p_b;
           ++nst;
         };
         tile(0, sr0, si0);
@@ -574,7 +578,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   }
 #ifdef SIDWT_TC_PROFILE
   if (p.prof && blockIdx.x == 0 && lane == 0 && (warp <= 2 || warp == kI8FirstEpi || warp == kI8Mma2 || warp == kI8FirstPeak))
-    printf("i8 cta0 warp %2d: total %lld wait %lld %lld %lld\n", warp, TC_CLOCK() - p_t0, pw[0], pw[1], pw[2]);
+    printf("i8 cta0 warp %2d: total %lld wait %lld %lld %lld %lld\n", warp, TC_CLOCK() - p_t0, pw[0], pw[1], pw[2], pw[3]);
 #endif
   tc_fence_before();
   __syncthreads();
