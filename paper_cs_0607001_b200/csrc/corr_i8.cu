@@ -471,27 +471,31 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
             for (int i = 0; i < PL / 2; ++i)
               dst[i] = make_int4((int)sr[2 * i], (int)si[2 * i], (int)sr[2 * i + 1], (int)si[2 * i + 1]);
           }
-          // corr_ti of this warp's 32 lag blocks -> swizzled staging (the TMA map's swizzle span =
-          // one lane's row); the buffer must have been read by the TMA store and the peak warp
+          // corr_ti of this warp's 32 lag blocks -> swizzled staging (64-byte rows, 16-byte chunks
+          // XOR-swizzled: conflict-free both ways) -> read back in store order -> coalesced
+          // 16-byte stores (8 x 64 B pieces per instruction).  The staging buffer is then read
+          // by the peak warp of this lane quarter; it must have finished with the buffer.
           const int b = nst & 1;
           unsigned char* sb = sbase + b * kI8StgBytes;
-          if (lane == 0) bulk_wait_read_le1();
           TC_TWAIT(&stgempty[2 * e + b], ((nst >> 1) & 1) ^ 1, pw[1]);
-          __syncwarp();
           constexpr int CH = kI8RowBytes / 16;                          // 16-byte chunks per row
           const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
 #pragma unroll
           for (int k = 0; k < CH; ++k)
             *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (k ^ sw)) =
                 make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
-          fence_proxy_async_smem();
-          mbar_arrive(&stgfull[2 * e + b]);
           __syncwarp();
-          if (want_corr && tma && lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: all in or all out
-            const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
-            tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
-            bulk_commit();
+          if (want_corr && tma && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's blocks all in or all out
+            int2* dst0 = corr + ((size_t)row * nterms + ti) * N + 2048 * t + 512 * quarter + 8 * h;
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+              const int piece = (32 / CH) * k + lane / CH, chunk = lane % CH;
+              const int psw = ((piece * kI8RowBytes) >> 7) & (CH - 1);
+              const int4 v = *reinterpret_cast<const int4*>(sb + kI8RowBytes * piece + 16 * (chunk ^ psw));
+              __stcs(reinterpret_cast<int4*>(dst0 + 16 * piece + 2 * chunk), v);
+            }
           }
+          mbar_arrive(&stgfull[2 * e + b]);
           pw[3] += TC_CLOCK() - p_b;
           ++nst;
         };
@@ -499,7 +503,6 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         if (ntiles > 1) tile(1, sr1, si1);
       }
     }
-    if (lane == 0) bulk_wait_all();
   } else if (warp >= kI8FirstPeak) {
     // ---------------- peak warps: warp k scans TMEM lane quarter k's staging (both halves: the 16
     // lags of lag block c in lane c), the row's peak per scale: smallest lag maximising |corr|^2
