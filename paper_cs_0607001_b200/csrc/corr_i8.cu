@@ -86,6 +86,14 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sa
 }
 __device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
 
+// non-blocking mbarrier phase test
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
 // D[tmem] (+)= A[smem] . B[smem], kind::i8 (int8 inputs, int32 accumulate)
 __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                         uint32_t accumulate) {
@@ -272,25 +280,36 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   const long long p_t0 = TC_CLOCK();
 
   if (warp == 0) {
-    // ---------------- loader: band segments (both components) and the term's B images
+    // ---------------- loader: band segments (both components) and the term's B images, the two
+    // rings advanced independently (non-blocking polls), so the band loads run as far ahead as
+    // their own ring allows
     if (lane == 0) {
-      uint32_t u = 0;
-      for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
-        for (int step = 0; step < nterms; ++step, ++u) {
+      const long long my_rows = p.rows > blockIdx.x ? (p.rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      const uint32_t total = (uint32_t)(my_rows * nterms);
+      uint32_t ub = 0, ui = 0;
+      while (ub < total || ui < total) {
+        if (ub < total && mbar_test(&bandempty[ub % NB], ((ub / NB) & 1) ^ 1)) {
+          const int step = (int)(ub % nterms);
+          const long long row = blockIdx.x + (long long)(ub / nterms) * gridDim.x;
           const I8Term& tm = p.term[step];
-          const uint32_t bs = u % NB, is = u % NI;
-          TC_TWAIT(&bandempty[bs], ((u / NB) & 1) ^ 1, pw[0]);
+          const uint32_t bs = ub % NB;
           const uint32_t bytes = (uint32_t)tm.seg_len * 4u;
           mbar_expect_tx(&bandfull[bs], 2 * bytes);
           const int* src = bands + ((size_t)row * nterms + tm.band) * 2 * p.stride + tm.seg_a4;
           int* dst = band + (size_t)bs * 2 * p.seg_alloc;
           bulk_load_g2s(dst, src, bytes, &bandfull[bs]);
           bulk_load_g2s(dst + p.seg_alloc, src + p.stride, bytes, &bandfull[bs]);
-          TC_TWAIT(&imgempty[is], ((u / NI) & 1) ^ 1, pw[1]);
+          ++ub;
+        }
+        if (ui < total && mbar_test(&imgempty[ui % NI], ((ui / NI) & 1) ^ 1)) {
+          const I8Term& tm = p.term[ui % nterms];
+          const uint32_t is = ui % NI;
           const uint32_t ib = (uint32_t)tm.ksteps * 2 * NCOL * 32;
           mbar_expect_tx(&imgfull[is], ib);
           bulk_load_g2s(imgs + (size_t)is * p.img_alloc, img + tm.img_ofs, ib, &imgfull[is]);
+          ++ui;
         }
+      }
     }
   } else if (warp == 1 || warp == kI8Mma2) {
     // ---------------- MMA issuers: two warps, warp k issues the MMAs of tiles t = k (mod 2) (one
@@ -471,31 +490,27 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
             for (int i = 0; i < PL / 2; ++i)
               dst[i] = make_int4((int)sr[2 * i], (int)si[2 * i], (int)sr[2 * i + 1], (int)si[2 * i + 1]);
           }
-          // corr_ti of this warp's 32 lag blocks -> swizzled staging (64-byte rows, 16-byte chunks
-          // XOR-swizzled: conflict-free both ways) -> read back in store order -> coalesced
-          // 16-byte stores (8 x 64 B pieces per instruction).  The staging buffer is then read
-          // by the peak warp of this lane quarter; it must have finished with the buffer.
+          // corr_ti of this warp's 32 lag blocks -> swizzled staging (the TMA map's swizzle span =
+          // one lane's row); the buffer must have been read by the TMA store and the peak warp
           const int b = nst & 1;
           unsigned char* sb = sbase + b * kI8StgBytes;
+          if (lane == 0) bulk_wait_read_le1();
           TC_TWAIT(&stgempty[2 * e + b], ((nst >> 1) & 1) ^ 1, pw[1]);
+          __syncwarp();
           constexpr int CH = kI8RowBytes / 16;                          // 16-byte chunks per row
           const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
 #pragma unroll
           for (int k = 0; k < CH; ++k)
             *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (k ^ sw)) =
                 make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
-          __syncwarp();
-          if (want_corr && tma && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's blocks all in or all out
-            int2* dst0 = corr + ((size_t)row * nterms + ti) * N + 2048 * t + 512 * quarter + 8 * h;
-#pragma unroll
-            for (int k = 0; k < CH; ++k) {
-              const int piece = (32 / CH) * k + lane / CH, chunk = lane % CH;
-              const int psw = ((piece * kI8RowBytes) >> 7) & (CH - 1);
-              const int4 v = *reinterpret_cast<const int4*>(sb + kI8RowBytes * piece + 16 * (chunk ^ psw));
-              __stcs(reinterpret_cast<int4*>(dst0 + 16 * piece + 2 * chunk), v);
-            }
-          }
+          fence_proxy_async_smem();
           mbar_arrive(&stgfull[2 * e + b]);
+          __syncwarp();
+          if (want_corr && tma && lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: all in or all out
+            const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
+            tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
+            bulk_commit();
+          }
           pw[3] += TC_CLOCK() - p_b;
           ++nst;
         };
@@ -503,6 +518,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         if (ntiles > 1) tile(1, sr1, si1);
       }
     }
+    if (lane == 0) bulk_wait_all();
   } else if (warp >= kI8FirstPeak) {
     // ---------------- peak warps: warp k scans TMEM lane quarter k's staging (both halves: the 16
     // lags of lag block c in lane c), the row's peak per scale: smallest lag maximising |corr|^2
