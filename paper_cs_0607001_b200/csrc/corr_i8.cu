@@ -48,7 +48,6 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <vector>
 
 namespace sidwt {
@@ -58,8 +57,7 @@ constexpr int kI8HW = 2, kI8PL = 16 / kI8HW;     // measured: 4 warps per quarte
 static_assert(kI8HW == 2, "accumulator column order n = 32 a + 16 (p / 8) + 8 oc + p % 8 assumes two halves");
 constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6, kI8EpiWarps = 4 * kI8HW;
 constexpr int kI8Mma2 = kI8FirstEpi + kI8EpiWarps;      // second MMA-issuing warp
-constexpr int kI8FirstPeak = kI8Mma2 + 1, kI8PeakWarps = 4;   // peak search: one warp per TMEM lane quarter
-constexpr int kI8Warps = kI8FirstPeak + kI8PeakWarps;
+constexpr int kI8Warps = kI8Mma2 + 1;
 constexpr int kI8Threads = 32 * kI8Warps;
 constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
 // TMEM: 512 columns, two accumulator buffers of 256 (tile t+1's MMAs overlap tile t's epilogue)
@@ -71,8 +69,8 @@ constexpr int kI8RowBytes = 8 * kI8PL;             // one lane's corr slice: kI8
 constexpr int kI8StgBytes = 32 * kI8RowBytes;       // per epilogue warp and buffer: 32 lag blocks
 __host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
   I8Smem L;
-  L.red = 1024;                                                         // [2 rows][J+1][kI8PeakWarps] peak partials
-  L.stg = (L.red + (size_t)2 * kI8MaxTerms * kI8PeakWarps * 24 + 1023) & ~(size_t)1023;  // swizzled TMA staging
+  L.red = 1024;                                                         // [2 rows][J+1][kI8EpiWarps] peak partials
+  L.stg = (L.red + (size_t)2 * kI8MaxTerms * kI8EpiWarps * 24 + 1023) & ~(size_t)1023;   // swizzled TMA staging
   L.band = L.stg + (size_t)kI8EpiWarps * 2 * kI8StgBytes;
   L.stream = (L.band + (size_t)p.nband * 2 * p.seg_alloc * 4 + 127) & ~(size_t)127;
   L.img = L.stream + (size_t)p.nstream * 2 * p.dmax * p.plane;
@@ -85,14 +83,6 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sa
                :: "l"(map), "r"(saddr), "r"(x0), "r"(x1), "r"(x2) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
-
-// non-blocking mbarrier phase test
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
-               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-  return ok != 0;
-}
 
 // D[tmem] (+)= A[smem] . B[smem], kind::i8 (int8 inputs, int32 accumulate)
 __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -244,12 +234,10 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   uint64_t* imgempty = imgfull + 4;                                   // [NI]
   uint64_t* dfull = imgempty + 4;                                     // [2]
   uint64_t* dempty = dfull + 2;                                       // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + 512);
-  int* dcnt = reinterpret_cast<int*>(smem_raw + 520);                 // [2] digits used per TMEM buffer
-  int* sflag = reinterpret_cast<int*>(smem_raw + 544);                // [4 stages][4 builder warps]
-  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + L.red);            // [2][kI8MaxTerms][kI8PeakWarps]
-  uint64_t* stgfull = dempty + 2;                                     // [kI8EpiWarps][2] staging written
-  uint64_t* stgempty = stgfull + 2 * kI8EpiWarps;                     // [kI8EpiWarps][2] staging read by the peak warp
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + 256);
+  int* dcnt = reinterpret_cast<int*>(smem_raw + 264);                 // [2] digits used per TMEM buffer
+  int* sflag = reinterpret_cast<int*>(smem_raw + 288);                // [4 stages][4 builder warps]
+  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + L.red);            // [2][kI8MaxTerms][kI8EpiWarps]
   unsigned char* stg = smem_raw + L.stg;                              // [kI8EpiWarps][2][kI8StgBytes]
   int* band = reinterpret_cast<int*>(smem_raw + L.band);
   unsigned char* stream = smem_raw + L.stream;
@@ -268,7 +256,6 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], nmma); }
     for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], nmma); }
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * kI8EpiWarps); }
-    for (int i = 0; i < 2 * kI8EpiWarps; ++i) { mbar_init(&stgfull[i], 32); mbar_init(&stgempty[i], 32); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tslot, kI8TmemCols);
@@ -276,40 +263,27 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  long long pw[4] = {0, 0, 0, 0};                                     // -DSIDWT_TC_PROFILE: wait / phase cycles per role
-  const long long p_t0 = TC_CLOCK();
 
   if (warp == 0) {
-    // ---------------- loader: band segments (both components) and the term's B images, the two
-    // rings advanced independently (non-blocking polls), so the band loads run as far ahead as
-    // their own ring allows
+    // ---------------- loader: band segments (both components) and the term's B images
     if (lane == 0) {
-      const long long my_rows = p.rows > blockIdx.x ? (p.rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-      const uint32_t total = (uint32_t)(my_rows * nterms);
-      uint32_t ub = 0, ui = 0;
-      while (ub < total || ui < total) {
-        if (ub < total && mbar_test(&bandempty[ub % NB], ((ub / NB) & 1) ^ 1)) {
-          const int step = (int)(ub % nterms);
-          const long long row = blockIdx.x + (long long)(ub / nterms) * gridDim.x;
+      uint32_t u = 0;
+      for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+        for (int step = 0; step < nterms; ++step, ++u) {
           const I8Term& tm = p.term[step];
-          const uint32_t bs = ub % NB;
+          const uint32_t bs = u % NB, is = u % NI;
+          mbar_wait(&bandempty[bs], ((u / NB) & 1) ^ 1);
           const uint32_t bytes = (uint32_t)tm.seg_len * 4u;
           mbar_expect_tx(&bandfull[bs], 2 * bytes);
           const int* src = bands + ((size_t)row * nterms + tm.band) * 2 * p.stride + tm.seg_a4;
           int* dst = band + (size_t)bs * 2 * p.seg_alloc;
           bulk_load_g2s(dst, src, bytes, &bandfull[bs]);
           bulk_load_g2s(dst + p.seg_alloc, src + p.stride, bytes, &bandfull[bs]);
-          ++ub;
-        }
-        if (ui < total && mbar_test(&imgempty[ui % NI], ((ui / NI) & 1) ^ 1)) {
-          const I8Term& tm = p.term[ui % nterms];
-          const uint32_t is = ui % NI;
+          mbar_wait(&imgempty[is], ((u / NI) & 1) ^ 1);
           const uint32_t ib = (uint32_t)tm.ksteps * 2 * NCOL * 32;
           mbar_expect_tx(&imgfull[is], ib);
           bulk_load_g2s(imgs + (size_t)is * p.img_alloc, img + tm.img_ofs, ib, &imgfull[is]);
-          ++ui;
         }
-      }
     }
   } else if (warp == 1 || warp == kI8Mma2) {
     // ---------------- MMA issuers: two warps, warp k issues the MMAs of tiles t = k (mod 2) (one
@@ -325,8 +299,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         const int ksteps = p.term[step].ksteps, kadv16 = p.term[step].kadv >> 4, dig = p.term[step].dig;
         const uint32_t ss = u % NS, is = u % NI;
         if (mw >= nmma) continue;                                          // single issuer: the second warp idles
-        TC_TWAIT(&sfull[ss], (u / NS) & 1, pw[0]);
-        TC_TWAIT(&imgfull[is], (u / NI) & 1, pw[1]);
+        mbar_wait(&sfull[ss], (u / NS) & 1);
+        mbar_wait(&imgfull[is], (u / NI) & 1);
         tc_fence_after();
         bool fits = true;
         for (int w = 0; w < kI8BuildWarps; ++w) fits = fits && sflag[ss * 4 + w] != 0;
@@ -336,7 +310,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         for (int t = 0; t < p.ntiles; ++t, ++q) {
           if (t % nmma != mw) continue;
           const uint32_t buf = q % NBUF;
-          TC_TWAIT(&dempty[buf], ((q / NBUF) & 1) ^ 1, pw[2]);
+          mbar_wait(&dempty[buf], ((q / NBUF) & 1) ^ 1);
           tc_fence_after();
           if (lane == 0) dcnt[buf] = D;
           __syncwarp();
@@ -366,8 +340,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       for (int step = 0; step < nterms; ++step, ++u) {
         const I8Term& tm = p.term[step];
         const uint32_t bs = u % NB, ss = u % NS;
-        TC_TWAIT(&bandfull[bs], (u / NB) & 1, pw[0]);
-        TC_TWAIT(&sempty[ss], ((u / NS) & 1) ^ 1, pw[1]);
+        mbar_wait(&bandfull[bs], (u / NB) & 1);
+        mbar_wait(&sempty[ss], ((u / NS) & 1) ^ 1);
         const int nd = tm.dig;
         const int n4 = tm.seg_len >> 2;
         unsigned range = 0;
@@ -422,8 +396,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         mbar_arrive(&bandempty[bs]);
       }
   } else if (warp < kI8FirstEpi + kI8EpiWarps) {
-    // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr staging
-    // (swizzled, one TMA tensor store per warp and tile); the peak warps scan the staging.
+    // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
     // kI8HW warps per TMEM lane quarter; warp h of a quarter takes shifts p = PL h .. PL h + PL-1
     // of every lag block, i.e. accumulator columns oc (16 TN) + h (PL TN) + a PL + pl.
     constexpr int PL = kI8PL, NC = kI8PL * TN;
@@ -433,17 +406,18 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     const int N = p.N, ntiles = p.ntiles;
     const bool want_corr = p.want_corr != 0, tma = p.tma_store != 0;
     unsigned char* sbase = stg + (size_t)(warp - kI8FirstEpi) * 2 * kI8StgBytes;
-    const int e = warp - kI8FirstEpi;
     uint32_t q = 0, nst = 0;
+    int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
       unsigned sr0[PL], si0[PL], sr1[PL], si1[PL];                      // running corr (mod 2^32) of tiles 0, 1
       for (int step = 0; step < nterms; ++step) {
         const int ti = p.J - step;
+        PeakI best;
+        best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
         // one tile: D_ti (digits recombined mod 2^32) added into the running sums (sr, si)
         auto tile = [&](int t, unsigned (&sr)[PL], unsigned (&si)[PL]) {
           const uint32_t buf = q % NBUF;
-          TC_TWAIT(&dfull[buf], (q / NBUF) & 1, pw[0]);
-          const long long p_a = TC_CLOCK();
+          mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
           const int D = dcnt[buf];
           // group c at columns 32 c + 16 h + [oc 8 + pl]: one x16 load per group
@@ -476,8 +450,6 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
           ++q;
-          const long long p_b = TC_CLOCK();
-          pw[2] += p_b - p_a;
           const int tau0 = 2048 * t + 16 * c + PL * h;
 #pragma unroll
           for (int i = 0; i < PL; ++i) {
@@ -490,84 +462,44 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
             for (int i = 0; i < PL / 2; ++i)
               dst[i] = make_int4((int)sr[2 * i], (int)si[2 * i], (int)sr[2 * i + 1], (int)si[2 * i + 1]);
           }
-          // corr_ti of this warp's 32 lag blocks -> swizzled staging (the TMA map's swizzle span =
-          // one lane's row); the buffer must have been read by the TMA store and the peak warp
-          const int b = nst & 1;
-          unsigned char* sb = sbase + b * kI8StgBytes;
-          if (lane == 0) bulk_wait_read_le1();
-          TC_TWAIT(&stgempty[2 * e + b], ((nst >> 1) & 1) ^ 1, pw[1]);
-          __syncwarp();
-          constexpr int CH = kI8RowBytes / 16;                          // 16-byte chunks per row
-          const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
+          if (want_corr && tma) {
+            // corr_ti of this warp's 32 lag blocks (PL lags each) -> swizzled staging (the TMA map's
+            // swizzle span = one lane's row) -> one TMA tensor store; the staging buffer of two
+            // stores ago must have been read
+            unsigned char* sb = sbase + (nst & 1) * kI8StgBytes;
+            if (lane == 0) bulk_wait_read_le1();
+            __syncwarp();
+            constexpr int CH = kI8RowBytes / 16;                        // 16-byte chunks per row
+            const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
 #pragma unroll
-          for (int k = 0; k < CH; ++k)
-            *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (k ^ sw)) =
-                make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
-          fence_proxy_async_smem();
-          mbar_arrive(&stgfull[2 * e + b]);
-          __syncwarp();
-          if (want_corr && tma && lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: all in or all out
-            const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
-            tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
-            bulk_commit();
+            for (int k = 0; k < CH; ++k)
+              *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (k ^ sw)) =
+                  make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's 32 blocks all in or all out
+              const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
+              tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
+              bulk_commit();
+            }
+            ++nst;
           }
-          pw[3] += TC_CLOCK() - p_b;
-          ++nst;
+          if (tau0 < N) {
+            // peak candidates in lag order: strict '>' keeps the smallest lag of a tie
+            if (best.tau < 0) { best.m2 = mag2i((int)sr[0], (int)si[0]); best.tau = tau0; best.re = (int)sr[0]; best.im = (int)si[0]; }
+#pragma unroll
+            for (int i = 0; i < PL; ++i) {
+              const unsigned long long m = mag2i((int)sr[i], (int)si[i]);
+              const bool gt = m > best.m2;
+              best.m2 = gt ? m : best.m2;
+              best.tau = gt ? tau0 + i : best.tau;
+              best.re = gt ? (int)sr[i] : best.re;
+              best.im = gt ? (int)si[i] : best.im;
+            }
+          }
         };
         tile(0, sr0, si0);
         if (ntiles > 1) tile(1, sr1, si1);
-      }
-    }
-    if (lane == 0) bulk_wait_all();
-  } else if (warp >= kI8FirstPeak) {
-    // ---------------- peak warps: warp k scans TMEM lane quarter k's staging (both halves: the 16
-    // lags of lag block c in lane c), the row's peak per scale: smallest lag maximising |corr|^2
-    const int k = warp - kI8FirstPeak;
-    const int e0 = (k + 4 - (kI8FirstEpi & 3)) & 3, e1 = e0 + 4;      // epilogue warps of quarter k (h = 0, 1)
-    const int c = 32 * k + lane;
-    const int N = p.N, ntiles = p.ntiles;
-    const int tp = threadIdx.x - 32 * kI8FirstPeak;
-    const unsigned char* sb0 = stg + (size_t)e0 * 2 * kI8StgBytes;
-    const unsigned char* sb1 = stg + (size_t)e1 * 2 * kI8StgBytes;
-    constexpr int CH = kI8RowBytes / 16;
-    const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
-    uint32_t nst = 0;
-    int par = 0;
-    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      for (int step = 0; step < nterms; ++step) {
-        const int ti = p.J - step;
-        PeakI best;
-        best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
-        for (int t = 0; t < ntiles; ++t, ++nst) {
-          const int b = nst & 1;
-          const uint32_t ph = (nst >> 1) & 1;
-          int4 v[2 * CH];
-          TC_TWAIT(&stgfull[2 * e0 + b], ph, pw[0]);
-#pragma unroll
-          for (int kk = 0; kk < CH; ++kk)
-            v[kk] = *reinterpret_cast<const int4*>(sb0 + b * kI8StgBytes + kI8RowBytes * lane + 16 * (kk ^ sw));
-          TC_TWAIT(&stgfull[2 * e1 + b], ph, pw[1]);
-#pragma unroll
-          for (int kk = 0; kk < CH; ++kk)
-            v[CH + kk] = *reinterpret_cast<const int4*>(sb1 + b * kI8StgBytes + kI8RowBytes * lane + 16 * (kk ^ sw));
-          mbar_arrive(&stgempty[2 * e0 + b]);
-          mbar_arrive(&stgempty[2 * e1 + b]);
-          const int tau0 = 2048 * t + 16 * c;
-          if (tau0 < N) {
-            // lags tau0 .. tau0 + 15 in order: strict '>' keeps the smallest lag of a tie
-            if (best.tau < 0) { best.m2 = mag2i(v[0].x, v[0].y); best.tau = tau0; best.re = v[0].x; best.im = v[0].y; }
-#pragma unroll
-            for (int i = 0; i < 2 * CH; ++i) {
-              const unsigned long long m0 = mag2i(v[i].x, v[i].y), m1 = mag2i(v[i].z, v[i].w);
-              const bool k0 = m0 >= m1;                                   // pair maximum, earlier lag on ties
-              const unsigned long long mx = k0 ? m0 : m1;
-              if (mx > best.m2) {
-                best.m2 = mx; best.tau = tau0 + 2 * i + (k0 ? 0 : 1);
-                best.re = k0 ? v[i].x : v[i].z; best.im = k0 ? v[i].y : v[i].w;
-              }
-            }
-          }
-        }
         // the row's peak at scale ti: warp argmax (high word, low word, smallest lag) -> partial
         const bool ok = best.tau >= 0;
         const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
@@ -575,30 +507,27 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
         const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
         const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
-        PeakI* rp = red + ((size_t)par * kI8MaxTerms + ti) * kI8PeakWarps;
-        if (ok && (unsigned)best.tau == tmin) rp[k] = best;
-        else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[k] = e; }
+        PeakI* rp = red + ((size_t)par * kI8MaxTerms + ti) * kI8EpiWarps;
+        if (ok && (unsigned)best.tau == tmin) rp[warp - kI8FirstEpi] = best;
+        else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[warp - kI8FirstEpi] = e; }
       }
-      // every scale of the row: combine the peak warps' partials (one barrier per row)
-      named_bar(2, 32 * kI8PeakWarps);
-      if (tp < nterms && lag) {
-        const PeakI* rp = red + ((size_t)par * kI8MaxTerms + tp) * kI8PeakWarps;
-        PeakI bb = rp[0];
-        for (int w = 1; w < kI8PeakWarps; ++w) {
+      // every scale of the row: combine the warps' partials (one barrier per row)
+      named_bar(2, 32 * kI8EpiWarps);
+      if (te < nterms && lag) {
+        const PeakI* rp = red + ((size_t)par * kI8MaxTerms + te) * kI8EpiWarps;
+        PeakI b = rp[0];
+        for (int w = 1; w < kI8EpiWarps; ++w) {
           const PeakI o = rp[w];
-          if (o.tau >= 0 && (bb.tau < 0 || beats(o.m2, o.tau, bb.m2, bb.tau))) bb = o;
+          if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
         }
-        const size_t ix = (size_t)row * nterms + tp;
-        lag[ix] = bb.tau;
-        if (val) val[ix] = make_int2(bb.re, bb.im);
+        const size_t e = (size_t)row * nterms + te;
+        lag[e] = b.tau;
+        if (val) val[e] = make_int2(b.re, b.im);
       }
       par ^= 1;
     }
+    if (lane == 0) bulk_wait_all();
   }
-#ifdef SIDWT_TC_PROFILE
-  if (p.prof && blockIdx.x == 0 && lane == 0 && (warp <= 2 || warp == kI8FirstEpi || warp == kI8Mma2 || warp == kI8FirstPeak))
-    printf("i8 cta0 warp %2d: total %lld wait %lld %lld %lld %lld\n", warp, TC_CLOCK() - p_t0, pw[0], pw[1], pw[2], pw[3]);
-#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, kI8TmemCols);
@@ -746,7 +675,6 @@ cudaError_t i8_launch(const I8Params& p0, const int* bands, const unsigned char*
                       int2* val, int grid, cudaStream_t s) {
   I8Params p = p0;
   p.tma_store = (p.N % 512 == 0) ? 1 : 0;
-  if (const char* ev = std::getenv("SIDWT_TC_PROF")) p.prof = atoi(ev);
   if (corr && p.tma_store && !encode_corr_map_i8(&p.cmap, corr, p.rows, p)) return cudaErrorInvalidValue;
   const size_t smem = i8_layout(p).total;
   void (*kern)(const int*, const unsigned char*, int2*, int32_t*, int2*, const I8Params);

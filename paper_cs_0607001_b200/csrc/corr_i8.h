@@ -34,7 +34,6 @@ struct I8Params {
   int seg_alloc, plane, img_alloc;    // int32 per component per band stage; bytes per digit plane; bytes per image stage
   int want_corr;
   int tma_store;                      // corr_s written by TMA tensor stores (N a multiple of 512), else st.global
-  int prof;                           // debug (-DSIDWT_TC_PROFILE, SIDWT_TC_PROF=1): CTA 0 prints role waits
   long long rows;
   I8Term term[kI8MaxTerms];           // by processing step (0 = coarsest, a_J)
 };
