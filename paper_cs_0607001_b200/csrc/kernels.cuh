@@ -198,8 +198,6 @@ struct AnaParams {
   Lift lift;
 };
 
-constexpr int kRVP = 7;        // K1 run length of the two-residue (8-byte access) levels, odd
-
 template <int FAM, int RV, int LH, bool BULK = true>
 __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict__ U, typename Dual<FAM>::T* __restrict__ Wst,
                                               int lbuf, const Lift& L) {
@@ -207,71 +205,30 @@ __device__ __forceinline__ void analyze_level(typename Dual<FAM>::T* __restrict_
   constexpr int HL = Dual<FAM>::HL, HR = Dual<FAM>::HR, WIN = RV + HL + HR;
   constexpr int h = 1 << LH;
   const int w = threadIdx.x;
-  if constexpr (LH >= 1 && BULK) {
-    // two adjacent residues (branches rho, rho + 1) per thread, runs of kRVP pairs: every
-    // shared-memory access is one 8-byte LDS / STS (half the instructions of the scalar form;
-    // conflict-free: kRVP odd); the second residue's extra position past lbuf falls into the
-    // zeroed pad
-    typedef typename std::conditional<std::is_same<T, int>::value, int2, float2>::type T2;
-    constexpr int RP = kRVP, WP = RP + HL + HR;
-    const int rho = (w & ((h >> 1) - 1)) << 1;
-    const int j0 = (w >> (LH - 1)) * RP;
-    const int len = (lbuf - rho + h - 1) >> LH;
-    const bool active = j0 < len;
-    const int u0 = rho + (j0 << LH);
-    T ca[RP], da[RP], cb[RP], db[RP];
-    if (active) {
-      const T* src = U + u0 - HL * h;
-      T va[WP], vb[WP];
+  const int rho = w & (h - 1);
+  const int j0 = (w >> LH) * RV;
+  const int len = (lbuf - rho + h - 1) >> LH;     // positions rho + h j < lbuf
+  const bool active = j0 < len;
+  const int u0 = rho + (j0 << LH);
+  T c[RV], d[RV];
+  if (active) {
+    const T* src = U + u0 - HL * h;
+    T v[WIN];
 #pragma unroll
-      for (int i = 0; i < WP; ++i) {
-        const T2 x = *reinterpret_cast<const T2*>(src + i * h);
-        va[i] = x.x;
-        vb[i] = x.y;
-      }
-      Dual<FAM>::template run<RP>(va, ca, da, L);
-      Dual<FAM>::template run<RP>(vb, cb, db, L);
-    }
-    if (threadIdx.x == 0) bulk_wait_read_all();   // staging free again
-    __syncthreads();
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < RP; ++i) {
-        T2 cu, dw;
-        cu.x = ca[i]; cu.y = cb[i];
-        dw.x = da[i]; dw.y = db[i];
-        *reinterpret_cast<T2*>(U + u0 + i * h) = cu;
-        *reinterpret_cast<T2*>(Wst + u0 + i * h) = dw;
-      }
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-  } else {
-    const int rho = w & (h - 1);
-    const int j0 = (w >> LH) * RV;
-    const int len = (lbuf - rho + h - 1) >> LH;     // positions rho + h j < lbuf
-    const bool active = j0 < len;
-    const int u0 = rho + (j0 << LH);
-    T c[RV], d[RV];
-    if (active) {
-      const T* src = U + u0 - HL * h;
-      T v[WIN];
-#pragma unroll
-      for (int i = 0; i < WIN; ++i) v[i] = src[i * h];
-      Dual<FAM>::template run<RV>(v, c, d, L);
-    }
-    if (BULK && threadIdx.x == 0 && LH > 0) bulk_wait_read_all();   // staging free again
-    __syncthreads();
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < RV; ++i) {
-        U[u0 + i * h] = c[i];
-        Wst[u0 + i * h] = d[i];
-      }
-    }
-    if (BULK) fence_proxy_async_smem();
-    __syncthreads();
+    for (int i = 0; i < WIN; ++i) v[i] = src[i * h];
+    Dual<FAM>::template run<RV>(v, c, d, L);
   }
+  if (BULK && threadIdx.x == 0 && LH > 0) bulk_wait_read_all();   // staging free again
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < RV; ++i) {
+      U[u0 + i * h] = c[i];
+      Wst[u0 + i * h] = d[i];
+    }
+  }
+  if (BULK) fence_proxy_async_smem();
+  __syncthreads();
 }
 
 // Levels LH = 0 .. J-1 as straight-line code (compile-time stride per level), each

@@ -190,16 +190,6 @@ int sidwt_template_is_real(sidwt_plan p) { return (p && p->loaded) ? (p->real_ta
 // Template load: supports, margins, tiling, and the device pyramid (K0).
 // ---------------------------------------------------------------------------
 static void k2_buffers(sidwt_plan_s* p, int Q);
-// K1 threads: level 1 (stride 1) lifts runs of kRV pairs of one residue per thread, levels
-// s >= 2 runs of kRVP pairs of two adjacent residues (kernels.cuh analyze_level)
-static int64_t ana_threads_for(int64_t lbuf, int J) {
-  int64_t threads = cdiv(lbuf, kRV);
-  for (int s = 2; s <= J; ++s) {
-    const int64_t h = 1LL << (s - 1);
-    threads = std::max(threads, (h / 2) * cdiv(cdiv(lbuf, h), kRVP));
-  }
-  return threads;
-}
 static void configure(sidwt_plan_s* p) {
   const int J = p->J;
   const Supp sp = analysis_support(p->fam);
@@ -264,7 +254,11 @@ static void configure(sidwt_plan_s* p) {
   for (;; ++ntiles) {
     tile_len = rup(cdiv(p->stride, ntiles), 32);
     lbuf = rup(halo_l + tile_len + halo_r, 4);
-    threads = ana_threads_for(lbuf, J);
+    threads = 0;
+    for (int s = 1; s <= J; ++s) {
+      const int64_t h = 1LL << (s - 1);
+      threads = std::max(threads, h * cdiv(cdiv(lbuf, h), kRV));
+    }
     if ((lbuf <= lbuf_target && threads <= 512) || tile_len <= 32) break;
   }
   // more, smaller tiles while the halo stays cheap (<= 5 % of the tile, tiles >= 2048 values):
@@ -275,7 +269,11 @@ static void configure(sidwt_plan_s* p) {
       const int64_t tl = rup(cdiv(p->stride, nt), 32);
       if (tl < 2048 || (halo_l + halo_r) * 20 > tl) break;
       ntiles = nt; tile_len = tl; lbuf = rup(halo_l + tile_len + halo_r, 4);
-      threads = ana_threads_for(lbuf, J);
+      threads = 0;
+      for (int s = 1; s <= J; ++s) {
+        const int64_t h = 1LL << (s - 1);
+        threads = std::max(threads, h * cdiv(cdiv(lbuf, h), kRV));
+      }
     }
   }
   ntiles = cdiv(p->stride, tile_len);
