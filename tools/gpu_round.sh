@@ -24,7 +24,7 @@ ncu_pair() {   # $1 suffix, $2 config, $3 rows for the full capture, $4 kernel r
   timeout 600 $CMD > $OUT/plain$1_$TAG.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches$1_$TAG.csv $CMD > $OUT/ncu_launch$1_$TAG.log 2>&1 && \
   timeout 300 $CMDR > $OUT/plainr$1_$TAG.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$4" -s 4 -c 2 -o $OUT/prof$1_$TAG $CMDR > $OUT/ncu_full$1_$TAG.log 2>&1
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$4" -s 4 -c 1 -o $OUT/prof$1_$TAG $CMDR > $OUT/ncu_full$1_$TAG.log 2>&1
   echo "ncu$1 rc=$?"
 }
 [ "$PART" = ncu ] && ncu_pair 5 5 4096 "k_analyze|k_correlate"
