@@ -24,13 +24,14 @@ ncu_pair() {   # $1 suffix, $2 config, $3 rows for the full capture, $4 kernel r
   timeout 600 $CMD > $OUT/plain$1_$TAG.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches$1_$TAG.csv $CMD > $OUT/ncu_launch$1_$TAG.log 2>&1 && \
   timeout 300 $CMDR > $OUT/plainr$1_$TAG.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$4" -s 4 -c 1 -o $OUT/prof$1_$TAG $CMDR > $OUT/ncu_full$1_$TAG.log 2>&1
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$4" -s 1 -c 1 -o $OUT/prof$1_$TAG $CMDR > $OUT/ncu_full$1_$TAG.log 2>&1
   echo "ncu$1 rc=$?"
 }
-[ "$PART" = ncu ] && ncu_pair 5 5 4096 "k_analyze|k_correlate"
-[ "$PART" = ncu2 ] && ncu_pair 2 2 4096 "k_analyze|k_correlate"
-[ "$PART" = ncu3 ] && ncu_pair 3 3 296 "k_analyze|k_correlate"
-[ "$PART" = ncu4 ] && ncu_pair 4 4 256 "k_analyze|k_correlate_tc"
+[ "$PART" = ncu ] && ncu_pair 5 5 4096 "k_correlate"
+[ "$PART" = ncu2 ] && ncu_pair 2 2 4096 "k_correlate"
+[ "$PART" = ncu3 ] && ncu_pair 3 3 296 "k_correlate"
+[ "$PART" = ncu4 ] && ncu_pair 4 4 256 "k_correlate_tc"
+[ "$PART" = ncuA ] && ncu_pair A${3:-5} ${3:-5} ${4:-4096} "k_analyze"
 if [ "$PART" = san ]; then
   TOOL=${3:-memcheck}
   timeout 1800 compute-sanitizer --tool $TOOL --error-exitcode 99 python -m pytest -q -x tests/test_gpu_sanitize.py \
