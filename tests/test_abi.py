@@ -47,6 +47,9 @@ def test_sass_is_sm100a(native):
     # single-template tensor-core correlation: tcgen05.mma, tcgen05.ld, bulk copies
     for k in ("UTCHMMA", "LDTM", "UBLKCP"):
         assert per["k_correlate_tcs"][k] > 0, ("k_correlate_tcs", k)
+    # integer family: int8 tcgen05.mma (UTCIMMA), tcgen05.ld, bulk loads, TMA tensor stores of corr
+    for k in ("UTCIMMA", "LDTM", "UTMASTG", "UBLKCP"):
+        assert per["k_correlate_i8"][k] > 0, ("k_correlate_i8", k)
     assert per["k_analyze"]["UBLKCP"] > 0                  # TMA bulk stores of the bands
     assert per["k_correlate"]["FFMA2"] > 0                 # packed FP32 real-template correlation
 
