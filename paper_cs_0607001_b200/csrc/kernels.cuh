@@ -282,34 +282,81 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
       return ext_index(n, N, p.ext);
     };
     constexpr int B = 8;
+    // interior positions [0, N) of the segment: 16-byte vector loads of 4 consecutive samples
+    // (both components) and one 16-byte shared store of this component's 4 values; the
+    // extension margins at the ends take the per-sample path below (needs Ai = 0 mod 4)
+    int v_lo = 0, v_hi = 0;
+    if ((Ai & 3) == 0) {
+      v_lo = (max(0, -Ai) + 3) & ~3;
+      v_hi = min(p.lbuf, N - Ai) & ~3;
+      if (v_hi < v_lo) v_hi = v_lo;
+      const int ngrp = (v_hi - v_lo) >> 2;
+      constexpr int G = 4;
+      for (int g0 = threadIdx.x; g0 < ngrp; g0 += G * blockDim.x) {
+        T x[G][4];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const int gi = g0 + k * blockDim.x;
+          const int u = v_lo + 4 * gi;
+          if (gi < ngrp) {
+            if constexpr (FAM == FI53) {
+              const int4 w = __ldg(reinterpret_cast<const int4*>(static_cast<const int16_t*>(rows_in) +
+                                                              ((size_t)row * p.N + (Ai + u)) * 2));
+              const int ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) x[k][e] = comp ? (ww[e] >> 16) : (int)(int16_t)(ww[e] & 0xffff);
+            } else {
+              const float4* q = reinterpret_cast<const float4*>(static_cast<const float*>(rows_in) +
+                                                                ((size_t)row * p.N + (Ai + u)) * 2);
+              const float4 a = __ldg(q), b = __ldg(q + 1);
+              x[k][0] = comp ? a.y : a.x; x[k][1] = comp ? a.w : a.z;
+              x[k][2] = comp ? b.y : b.x; x[k][3] = comp ? b.w : b.z;
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const int gi = g0 + k * blockDim.x;
+          if (gi < ngrp) {
+            typedef typename std::conditional<FAM == FI53, int4, float4>::type T4;
+            T4 o;
+            o.x = x[k][0]; o.y = x[k][1]; o.z = x[k][2]; o.w = x[k][3];
+            *reinterpret_cast<T4*>(U + v_lo + 4 * gi) = o;
+          }
+        }
+      }
+    }
+    // the rest (extension margins, or everything when Ai is not a multiple of 4): per sample
+    const int nrest = p.lbuf - (v_hi - v_lo);
+    auto rest_u = [&](int i) -> int { return i < v_lo ? i : i + (v_hi - v_lo); };
     if constexpr (FAM == FI53) {
       const int16_t* src = static_cast<const int16_t*>(rows_in) + (size_t)row * p.N * 2 + comp;
-      for (int u0 = threadIdx.x; u0 < p.lbuf; u0 += B * blockDim.x) {
+      for (int i0 = threadIdx.x; i0 < nrest; i0 += B * blockDim.x) {
         T v[B];
 #pragma unroll
         for (int k = 0; k < B; ++k) {
-          const int u = u0 + k * blockDim.x;
-          v[k] = u < p.lbuf ? (T)__ldg(src + 2 * (size_t)src_index(u)) : T(0);
+          const int i = i0 + k * blockDim.x;
+          v[k] = i < nrest ? (T)__ldg(src + 2 * (size_t)src_index(rest_u(i))) : T(0);
         }
 #pragma unroll
         for (int k = 0; k < B; ++k) {
-          const int u = u0 + k * blockDim.x;
-          if (u < p.lbuf) U[u] = v[k];
+          const int i = i0 + k * blockDim.x;
+          if (i < nrest) U[rest_u(i)] = v[k];
         }
       }
     } else {
       const float* src = static_cast<const float*>(rows_in) + (size_t)row * p.N * 2 + comp;
-      for (int u0 = threadIdx.x; u0 < p.lbuf; u0 += B * blockDim.x) {
+      for (int i0 = threadIdx.x; i0 < nrest; i0 += B * blockDim.x) {
         T v[B];
 #pragma unroll
         for (int k = 0; k < B; ++k) {
-          const int u = u0 + k * blockDim.x;
-          v[k] = u < p.lbuf ? __ldg(src + 2 * (size_t)src_index(u)) : T(0);
+          const int i = i0 + k * blockDim.x;
+          v[k] = i < nrest ? __ldg(src + 2 * (size_t)src_index(rest_u(i))) : T(0);
         }
 #pragma unroll
         for (int k = 0; k < B; ++k) {
-          const int u = u0 + k * blockDim.x;
-          if (u < p.lbuf) U[u] = v[k];
+          const int i = i0 + k * blockDim.x;
+          if (i < nrest) U[rest_u(i)] = v[k];
         }
       }
     }
