@@ -264,9 +264,15 @@ __global__ void __launch_bounds__(512) k_analyze(const void* __restrict__ rows_i
   const int out_len = min(p.tile_len, p.stride - tstart);
   const long long A = (long long)(-p.ML + tstart) - p.halo_l;
 
-  // zero the pads (reads past the buffer ends see finite values)
-  for (int u = threadIdx.x; u < p.padl; u += blockDim.x) Ubuf[u] = T(0);
-  for (int u = threadIdx.x; u < p.padr; u += blockDim.x) U[p.lbuf + u] = T(0);
+  // zero the pads (reads past the buffer ends see finite values); 16-byte stores (padl, padr,
+  // lbuf are multiples of 4)
+  {
+    typedef typename std::conditional<FAM == FI53, int4, float4>::type T4;
+    T4 z;
+    z.x = T(0); z.y = T(0); z.z = T(0); z.w = T(0);
+    for (int u = threadIdx.x; u < (p.padl >> 2); u += blockDim.x) reinterpret_cast<T4*>(Ubuf)[u] = z;
+    for (int u = threadIdx.x; u < (p.padr >> 2); u += blockDim.x) reinterpret_cast<T4*>(U + p.lbuf)[u] = z;
+  }
   // load the extended row segment (one component); 8 independent loads in flight per thread
   {
     const int N = p.N;
