@@ -99,6 +99,12 @@ __global__ void k_tcs_images(const float2* __restrict__ taps, TcsParams p, int t
   }
 }
 
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n" : "=r"(pred));
+  return pred != 0;
+}
+
 // Pipeline stages: a term's K steps are taken plane by plane (all re-plane K steps, then all
 // im-plane ones), two K steps per stage, so the band segment of one plane can be reloaded for
 // the next term while the other plane is being processed.  Stage s of a term with ksteps K
@@ -258,56 +264,63 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
       if (p.prof && blockIdx.x == 0) printf("tcs cta0 producer: wait aempty %lld\n", w_a);
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
+    // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform values stay in
+    // uniform registers), one elected lane issues the MMAs and the commits
+    {
       const uint32_t idesc0 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.ncols >> 3) << 17) |
                               ((uint32_t)(128 >> 4) << 24);
+      const uint32_t idesc2 = (idesc0 & ~(0x3Fu << 17)) | ((uint32_t)((2 * p.ncols) >> 3) << 17);
+      const bool merged = p.merged != 0;
       uint32_t q = 0, qb = 0, qd = 0;
       long long w_d = 0, w_af = 0, w_bf = 0;
       const long long t_start = TC_CLOCK();
       const uint32_t ring0 = smem_u32(ring), bst0 = smem_u32(bst);
+      // descriptors differ only in their start address: precompute the fixed fields once
+      const uint64_t dA = smem_desc(ring0, 128, 256), dB = smem_desc(bst0, 128, 256);
+      const uint32_t bblock16 = (uint32_t)bblock >> 4, bstage16 = (uint32_t)bstage >> 4;
       for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
         for (int step = 0; step < nterms; ++step, ++qd) {
-          const TcsTerm& tm = p.term[step];
+          const int nsp = tcs_nsp(p.term[step].ksteps);
+          const int ksteps = p.term[step].ksteps;
           const uint32_t db = qd & 1, dph = (qd >> 1) & 1;
           TC_TWAIT(&dempty[db], dph ^ 1, w_d);
           tc_fence_after();
           const uint32_t dt = tmem + db * p.ncols_alloc;
-          const uint32_t idesc = idesc0;
-          const bool merged = p.merged != 0;
-          const uint32_t idesc2 = (idesc0 & ~(0x3Fu << 17)) | ((uint32_t)((2 * p.ncols) >> 3) << 17);
-          const int nsp = tcs_nsp(tm.ksteps);
           for (int st = 0; st < 2 * nsp; ++st, ++q, ++qb) {
-            const int kc = min(2, tm.ksteps - 2 * (st % nsp));
+            const int kc = min(2, ksteps - 2 * (st % nsp));
             const uint32_t slot = q % S, ph = (q / S) & 1;
             const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
             TC_TWAIT(&afull[slot], ph, w_af);
             TC_TWAIT(&bfull[bs], bph, w_bf);
             tc_fence_after();
-            const uint32_t a0 = ring0 + slot * kTcsAStage, b0 = bst0 + bs * bstage;
-            for (int kk = 0; kk < kc; ++kk) {
-              const uint64_t ahi = smem_desc(a0 + kk * 8192, 128, 256);
-              const uint64_t alo = smem_desc(a0 + kk * 8192 + 4096, 128, 256);
-              const uint64_t bhi = smem_desc(b0 + kk * 2 * bblock, 128, 256);
-              const uint32_t acc0 = (st > 0 || kk > 0) ? 1u : 0u;
-              if (merged) {
-                // D[:, 0:nc] += A_hi B_hi and D[:, nc:2nc] += A_hi B_lo in one MMA over the adjacent
-                // hi | lo blocks (N = 2 nc, A_hi read once), then D[:, 0:nc] += A_lo B_hi
-                umma_bf16(dt, ahi, bhi, idesc2, acc0);
-                umma_bf16(dt, alo, bhi, idesc, 1u);
-              } else {
-                const uint64_t blo = smem_desc(b0 + kk * 2 * bblock + bblock, 128, 256);
-                umma_bf16(dt, ahi, bhi, idesc, acc0);
-                umma_bf16(dt, ahi, blo, idesc, 1u);
-                umma_bf16(dt, alo, bhi, idesc, 1u);
+            if (elect_one_sync()) {
+              const uint64_t a0 = dA + (uint64_t)(slot * (kTcsAStage >> 4)), b0 = dB + (uint64_t)(bs * bstage16);
+              for (int kk = 0; kk < kc; ++kk) {
+                const uint64_t ahi = a0 + (uint64_t)(kk * (8192 >> 4));
+                const uint64_t alo = ahi + (uint64_t)(4096 >> 4);
+                const uint64_t bhi = b0 + (uint64_t)(kk * 2 * bblock16);
+                const uint32_t acc0 = (st > 0 || kk > 0) ? 1u : 0u;
+                if (merged) {
+                  // D[:, 0:nc] += A_hi B_hi and D[:, nc:2nc] += A_hi B_lo in one MMA over the adjacent
+                  // hi | lo blocks (N = 2 nc, A_hi read once), then D[:, 0:nc] += A_lo B_hi
+                  umma_bf16(dt, ahi, bhi, idesc2, acc0);
+                  umma_bf16(dt, alo, bhi, idesc0, 1u);
+                } else {
+                  const uint64_t blo = bhi + (uint64_t)bblock16;
+                  umma_bf16(dt, ahi, bhi, idesc0, acc0);
+                  umma_bf16(dt, ahi, blo, idesc0, 1u);
+                  umma_bf16(dt, alo, bhi, idesc0, 1u);
+                }
               }
+              umma_commit(&aempty[slot]);
+              umma_commit(&bempty[bs]);
             }
-            umma_commit(&aempty[slot]);
-            umma_commit(&bempty[bs]);
+            __syncwarp();
           }
-          umma_commit(&dfull[db]);
+          if (elect_one_sync()) umma_commit(&dfull[db]);
+          __syncwarp();
         }
-      if (p.prof && blockIdx.x == 0)
+      if (p.prof && blockIdx.x == 0 && lane == 0)
         printf("tcs cta0 mma: total %lld wait dempty %lld afull %lld bfull %lld\n", TC_CLOCK() - t_start, w_d, w_af, w_bf);
     }
   } else if (warp < kTcsFirstEpi) {
