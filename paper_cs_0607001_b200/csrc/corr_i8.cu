@@ -131,15 +131,6 @@ __device__ __forceinline__ void tie_regs(uint32_t (&r)[NR]) {   // uses of r are
   for (int i = 0; i < NR; ++i) asm volatile("" : "+r"(r[i]));
 }
 
-// Ampere-style asynchronous 16-byte copy global -> shared (LSU path), and the arrival on an
-// mbarrier once all of this thread's prior cp.async have landed (the count is not incremented)
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(smem_u32(sdst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" :: "r"(smem_u32(bar)) : "memory");
-}
-
 // 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread (no wait)
 __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
@@ -261,7 +252,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   // two MMA-issuing warps (one tile each) when a row has two tiles and TMEM is double-buffered
   const int nmma = (p.ntiles >= 2 && NBUF == 2) ? 2 : 1;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) { mbar_init(&bandfull[i], 32); mbar_init(&bandempty[i], kI8BuildThreads); }
+    for (int i = 0; i < NB; ++i) { mbar_init(&bandfull[i], 1); mbar_init(&bandempty[i], kI8BuildThreads); }
     for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], nmma); }
     for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], nmma); }
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * kI8EpiWarps); }
@@ -274,31 +265,26 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
-    // ---------------- loader: band segments (both components) by 16-byte cp.async of the whole
-    // warp (the LSU path: the TMA engine stays free for the epilogue's corr stores), completion
-    // signalled per lane on bandfull; the term's B images by one bulk copy
-    uint32_t u = 0;
-    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
-      for (int step = 0; step < nterms; ++step, ++u) {
-        const I8Term& tm = p.term[step];
-        const uint32_t bs = u % NB, is = u % NI;
-        mbar_wait(&bandempty[bs], ((u / NB) & 1) ^ 1);
-        const int n16 = tm.seg_len >> 2;                                  // 16-byte chunks per component
-        const int* src = bands + ((size_t)row * nterms + tm.band) * 2 * p.stride + tm.seg_a4;
-        int* dst = band + (size_t)bs * 2 * p.seg_alloc;
-        for (int i = lane; i < 2 * n16; i += 32) {
-          const int x = i >= n16 ? 1 : 0, c = i - x * n16;
-          cp_async16(dst + (size_t)x * p.seg_alloc + 4 * c, src + (size_t)x * p.stride + 4 * c);
-        }
-        cp_async_arrive_noinc(&bandfull[bs]);
-        if (lane == 0) {
+    // ---------------- loader: band segments (both components) and the term's B images
+    if (lane == 0) {
+      uint32_t u = 0;
+      for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+        for (int step = 0; step < nterms; ++step, ++u) {
+          const I8Term& tm = p.term[step];
+          const uint32_t bs = u % NB, is = u % NI;
+          mbar_wait(&bandempty[bs], ((u / NB) & 1) ^ 1);
+          const uint32_t bytes = (uint32_t)tm.seg_len * 4u;
+          mbar_expect_tx(&bandfull[bs], 2 * bytes);
+          const int* src = bands + ((size_t)row * nterms + tm.band) * 2 * p.stride + tm.seg_a4;
+          int* dst = band + (size_t)bs * 2 * p.seg_alloc;
+          bulk_load_g2s(dst, src, bytes, &bandfull[bs]);
+          bulk_load_g2s(dst + p.seg_alloc, src + p.stride, bytes, &bandfull[bs]);
           mbar_wait(&imgempty[is], ((u / NI) & 1) ^ 1);
           const uint32_t ib = (uint32_t)tm.ksteps * 2 * NCOL * 32;
           mbar_expect_tx(&imgfull[is], ib);
           bulk_load_g2s(imgs + (size_t)is * p.img_alloc, img + tm.img_ofs, ib, &imgfull[is]);
         }
-        __syncwarp();
-      }
+    }
   } else if (warp == 1 || warp == kI8Mma2) {
     // ---------------- MMA issuers: two warps, warp k issues the MMAs of tiles t = k (mod 2) (one
     // tile per warp for N = 4096), so the two tiles' issue latencies overlap.  The whole warp runs
