@@ -5,70 +5,106 @@
 // Term i (band W at stride g = 2^lg, taps b[k] at support positions kmin + k, k < n):
 //     D[tau] = sum_k conj(b[k]) W[tau + g (kmin + k)]          (a5)
 // Within residue class r (tau = r + g q) this is an ordinary correlation of the
-// decimated sequence u_r[j] = W[r + g (kmin + j)] with the template.  Blocks of 64
-// consecutive q form one GEMM column: with q = 64 blk + p,
-//     D[r + g (64 blk + p)] = sum_j A[p][j] u_r[64 blk + j],   A[p][j] = conj(b[j - p])
-// so A (M = 128 rows = 64 shifts p x (re, im)) is the template's Toeplitz matrix,
-// shared by every row, term-wise constant, and precomputed once (image in global
-// memory, streamed through a shared-memory ring by bulk copies); B (N = one column per
-// (blk, r), N / 64 columns per row) is the band gathered at stride g, built in shared
-// memory per K step by builder warps from the term's band segment; K runs over
-// j in [0, n + 63) (padded to 16) for the re plane then the im plane.  fp32 operands
-// are split into bf16 hi + lo; three MMAs (hi.hi + hi.lo + lo.hi) per plane and K step
-// accumulate in fp32 in TMEM (same precision scheme as corr_tc.cuh).
+// decimated sequence u_r[j] = W[r + g (kmin + j)] with the template (the paper's even/odd
+// branch sequences).  Blocks of 64 consecutive q form one data
+// row of the GEMM: with q = 64 blk + p,
+//     D[r + g (64 blk + p)] = sum_j u_r[64 blk + j] T[p][j],   T[p][j] = conj(b[j - p])
+// so the M side (128 rows, one per n = blk g + r, N / 64 of them per row) is the band read
+// at stride g, and the N side (64 shifts p x (re, im) = 128 columns, interleaved 2 p + c) is
+// the template's Toeplitz matrix -- shared by every row, term-wise constant, precomputed
+// once (image in global memory, streamed through a shared-memory ring by bulk copies).
+// K runs over j in [0, n + 63) (padded to 16) for the re plane, then the im plane.  fp32
+// operands are split into bf16 hi + lo; per plane and K step two MMAs accumulate in fp32
+// in TMEM: data_hi x [T_hi | T_lo] (N = 256: the template's hi and lo images are adjacent,
+// so data_hi is read once for both) and data_lo x T_hi (N = 128), i.e. hi.hi + hi.lo + lo.hi
+// (the precision scheme of corr_tc.cuh).
 //
-// Eq. (4): one CTA owns a whole row (persistent over rows) and takes
-// the terms coarsest first; the row's running corr lives in shared memory: the epilogue
-// of term i adds D_i to it (acc = corr_{i+1} + D_i = corr_i), tracks the row's peak for
-// that scale (a7) -- so no peak partials and no finalize kernel -- and one bulk copy
-// stores corr_i (none in the peaks-only mode).
+// The data operand without per-K-step building.  A[n][k] = u_r[64 blk + k] is a Hankel
+// matrix in (blk, k): K step ks (k = 16 ks + kk) of row n reads the same values as
+// K step ks - 4 of row n + g.  So one buffer per (term, plane, split) holds every
+// value once, as 16-byte rows R[kc][n'] = u_r[64 blk' + 8 kc + e], e < 8 (n' = blk' g + r,
+// kc < 8 the 8-tap chunk inside a 64-tap window, n' up to ncols + g X_kc), and the
+// operand of K step ks = 4 X + i is the canonical K-major no-swizzle view starting at
+// row (2 i, X g) with SBO = 128 B (8 consecutive rows) and LBO = the distance of chunk
+// planes 2 i and 2 i + 1.  Converter warps fill the buffer once per (term, plane) with
+// coalesced loads of the fine-grid band from global memory (a permutation of the
+// band segment, no duplication), split into hi / lo bf16; the MMA then runs all K steps
+// of the plane from it.  Two buffers (one per plane) let a plane of the next term be
+// converted while the other is multiplied.
 //
-// Roles (448 threads):  warp 0 template-operand producer (bulk copies of image stages);
-// warp 1 MMA issuer (one thread); warps 2-9 builders (+ the band segment loader);
-// warps 10-13 epilogue (TMEM -> staging -> corr, four lane quarters of TMEM).
+// Eq. (4) and the peaks in one epilogue pass.  TMEM lane n holds the
+// data row (blk, r): 64 consecutive lags of residue class r, re and im side by side.  One
+// CTA owns a whole row (persistent over rows) and takes the terms coarsest first; the
+// row's running corr lives in shared memory (complex, one float2 of padding per 64 lags,
+// so the lanes of a warp hit different banks for every g).  The epilogue of term i adds
+// D_i to it (acc = corr_{i+1} + D_i = corr_i) straight from the TMEM registers, tracks the
+// row's peak at that scale (a7) on the same values -- no peak partials, no finalize
+// kernel -- and writes corr_i (none in the peaks-only mode).
+//
+// Roles (512 threads):  warp 0 template-operand producer (bulk copies of image stages);
+// warp 1 MMA issuer (the warp runs the loop, one elected lane issues); warps 2-4 convert
+// the re plane, warps 5-7 the im plane; warps 8-15 epilogue (two warps per TMEM lane
+// quarter: shifts p < 32 and p >= 32).
 #pragma once
 #include "corr_tc.cuh"
 
 namespace sidwt {
 
-constexpr int kTcsWarps = 14;
+constexpr int kTcsWarps = 16;
 constexpr int kTcsThreads = 32 * kTcsWarps;
-constexpr int kTcsFirstBuild = 2, kTcsBuildWarps = 8;
-constexpr int kTcsFirstEpi = 10;
+constexpr int kTcsFirstConv = 2, kTcsConvWarps = 6;     // 3 warps (96 threads) per plane
+constexpr int kTcsConvThreads = 96;
+constexpr int kTcsFirstEpi = 8, kTcsEpiWarps = 8, kTcsEpiThreads = 32 * kTcsEpiWarps;
 constexpr int kTcsAStage = 16384;               // one K step: 2 planes x (hi, lo) x 128 rows x 16 x bf16
 
 struct TcsTerm {
   int band, lg, kmin, ntap, toff;
   int ksteps, kofs;                             // K steps (16 taps each) and first K step in the image
-  int pos_lo;                                   // first fine-grid position of the term's band segment
-  int a4;                                       // band index (pos + ML) of the segment start, 16-byte aligned
-  int seg_len;                                  // floats loaded per plane (multiple of 4)
-  int pad;                                      // shared-memory padding (floats) after every 64 g positions
+  int kcoff[9];                                 // first buffer row of chunk plane kc (kcoff[8] = rows per split)
 };
 
 struct TcsParams {
-  int N, J, stride, ML, ncols, ncols_alloc, stages, seg_alloc;
+  int N, J, stride, ML, ncols, ncols_alloc, stages, brows_max;
   int want_corr;
-  int merged;                                   // 1: hi | lo B products merged into one N = 2 ncols MMA
   int prof;                                     // debug (-DSIDWT_TC_PROFILE, SIDWT_TC_PROF=1): CTA 0 prints role waits
   long long rows;
   TcsTerm term[17];                             // indexed by processing step (0 = coarsest, A_J)
 };
 
-struct TcsSmem { size_t bars, ring, bst, stg, band, acc, total; };
+// buffer rows of a term: chunk plane kc holds n' in [0, ncols + g X_kc), X_kc the largest
+// column shift (ks / 4) of the K steps ks = 4 X + kc / 2 that read it (none: empty plane)
+__host__ __device__ inline void tcs_term_rows(TcsTerm& tm, int ncols) {
+  const int g = 1 << tm.lg;
+  int o = 0;
+  for (int kc = 0; kc < 8; ++kc) {
+    int X = -1;
+    for (int ks = 0; ks < tm.ksteps; ++ks)
+      if ((ks & 3) == (kc >> 1)) X = ks >> 2;
+    tm.kcoff[kc] = o;
+    o += X < 0 ? 0 : ncols + g * X;
+  }
+  tm.kcoff[8] = o;
+}
+
+// padded position of lag tau in the running corr (float2 units): one float2 of padding per 64
+// lags, so that the 16 lanes of a 64-bit shared-memory phase (16 consecutive data rows n =
+// blk g + r, same shift p) fall on different banks for every g; a thread's run of 8 shifts
+// is a base plus compile-time offsets
+__host__ __device__ __forceinline__ int tcs_pad(int tau) { return tau + (tau >> 6); }
+
+struct TcsSmem { size_t bars, ring, bbuf, bslot, acc, total; };
 __host__ __device__ inline TcsSmem tcs_smem_layout(const TcsParams& p) {
   TcsSmem L;
   L.bars = 0;
   L.ring = 1024;
-  L.bst = L.ring + (size_t)p.stages * kTcsAStage;
-  L.stg = L.bst + (size_t)2 * p.ncols * 128;      // two B stages of ncols x 16 x 2 planes x 2 splits x bf16
-  L.band = L.stg + 128 * 32 * 4;
-  L.acc = L.band + (size_t)2 * p.seg_alloc * 4;
-  L.total = L.acc + (size_t)p.N * 8;              // the row's running corr (eq. (4) suffix sum)
+  L.bbuf = L.ring + (size_t)p.stages * kTcsAStage;
+  L.bslot = (size_t)2 * p.brows_max * 16;         // one plane: (hi, lo) x rows x 16 B
+  L.acc = L.bbuf + 2 * L.bslot;
+  L.total = L.acc + (size_t)(tcs_pad(p.N) + 2) * 8;   // the row's running corr (eq. (4) suffix sum), float2
   return L;
 }
 
-// Template Toeplitz images: img[kofs + ks][plane][split][4096 B], rows m = 64 c + p,
+// Template Toeplitz images: img[kofs + ks][plane][split][4096 B], rows m = 2 p + c,
 // K-major no-swizzle core matrices ((m, kk) at (m/8)*256 + (kk/8)*128 + (m%8)*16 + (kk%8)*2).
 // conj(b) w = (br wr + bi wi) + i (br wi - bi wr): row (p, re) = (br | bi), (p, im) = (-bi | br).
 __global__ void k_tcs_images(const float2* __restrict__ taps, TcsParams p, int total_ksteps,
@@ -83,7 +119,7 @@ __global__ void k_tcs_images(const float2* __restrict__ taps, TcsParams p, int t
   while (step < p.J && q >= p.term[step + 1].kofs) ++step;
   const TcsTerm tm = p.term[step];
   const int ks = q - tm.kofs;
-  const int c = m >> 6, pp = m & 63;
+  const int c = m & 1, pp = m >> 1;
   unsigned char* blk = img + ((size_t)q * 4 + plane * 2 + split) * 4096;
   for (int kk = 0; kk < 16; ++kk) {
     const int k = 16 * ks + kk - pp;            // template tap index
@@ -105,84 +141,148 @@ __device__ __forceinline__ bool elect_one_sync() {
   return pred != 0;
 }
 
-// Pipeline stages: a term's K steps are taken plane by plane (all re-plane K steps, then all
-// im-plane ones), two K steps per stage, so the band segment of one plane can be reloaded for
-// the next term while the other plane is being processed.  Stage s of a term with ksteps K
-// steps: plane s / nsp, K steps 2 (s % nsp) + {0, 1} (the last stage of a plane may hold one).
+
+// Pipeline stages of the template operand: a term's K steps are taken plane by plane (all
+// re-plane K steps, then all im-plane ones), two K steps per stage.  Stage s of a term with
+// ksteps K steps: plane s / nsp, K steps 2 (s % nsp) + {0, 1} (the last stage of a plane may
+// hold one).
 __host__ __device__ inline int tcs_nsp(int ksteps) { return (ksteps + 1) >> 1; }
 
-// Builders: the B operand of one plane's stages (K-major bf16 hi / lo blocks).  Thread chunk
-// (n, h, kk) = taps j = 16 (2 kp + kk) + 8 h + e (e < 8) of column n = blk g + r: position
-// r + g (64 blk + kmin + j), segment index off0 + r + g (64 blk + j), shared-memory index
-// idx + pad (idx >> (lg + 6)).  LG >= 0 makes the stride a compile-time constant.  Software
-// pipelined: the band values of the next stage are loaded right after a stage is handed over.
-template <int LG>
-__device__ __forceinline__ void tcs_build_phase(const TcsParams& p, const TcsTerm& tm, int tb, const float* src,
-                                                unsigned char* bst, uint64_t* bfull, uint64_t* bempty, uint32_t& qb,
-                                                long long& w_be, long long& t_build) {
-  constexpr int U = 2;                                        // chunks per thread per stage
-  const int lg = LG >= 0 ? LG : tm.lg;
-  const int g = 1 << lg, sh = lg + 6;
-  const int off0 = tm.pos_lo + p.ML - tm.a4;                  // segment index of position pos_lo
-  const int lim = p.stride - tm.a4;                           // segment indices >= lim are past the band
-  const int bstage = p.ncols * 128, bblock = p.ncols * 32;
-  const int nsp = tcs_nsp(tm.ksteps);
-  int base[U], oo[U], kks[U];
+// Converter: one plane of one term -> buffer rows (hi block, then lo block).  Rows come in
+// groups of V = min(4, g) consecutive residues r (same kc, same blk'): their band positions
+// r + g (kmin + 64 blk' + 8 kc + e) are V consecutive floats for every e, so a group is
+// 8 vector loads from global memory (coalesced across the warp) and 2 V 16-byte shared
+// stores.  Thread tc takes groups q = tc + 96 b.  A round is G groups (3 of 4 rows or 4 of
+// 2: at most 96 floats in registers); the first round -- for C3 the whole term-plane when
+// g >= 4 -- is loaded before waiting for the buffer, so the load latency overlaps the MMAs
+// still reading it.  Positions at or past the band stride meet zero Toeplitz entries: their
+// loads are clamped to the last in-band vector (finite values; V divides idx and stride).
+template <int V>
+__device__ __forceinline__ void tcs_convert(const TcsParams& p, const TcsTerm& tm, int tc, const float* __restrict__ src,
+                                            unsigned char* buf, uint64_t* bfull, uint64_t* bempty, uint32_t par,
+                                            long long& w_be) {
+  constexpr int G = 2;
+  const int lg = tm.lg;
+  const int g = 1 << lg;
+  const int brows = tm.kcoff[8];
+  const int nq = brows / V;                                   // every chunk plane has a multiple of 4 rows
+  const int base = p.ML + g * tm.kmin;                        // band index of (r = 0, m = 0), a multiple of V
+  const int lim = p.stride - V;
+  // register slot k of a group holds residue row (k + rot) % V, rot = (lane / (8 / V)) % V: the 8
+  // lanes of a 16-byte store phase then write 8 different 16-byte slots (conflict-free)
+  const int rot = (tc >> (V == 4 ? 1 : 2)) & (V - 1);
+  auto load = [&](int b, float (&v)[8][V]) {
+    const int q = tc + kTcsConvThreads * b;
+    if (q < nq) {
+      const int t = q * V;
+      int kc = 0;
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int ci = tb + u * 32 * kTcsBuildWarps;
-    const int n = ci % p.ncols;
-    const int h = (ci / p.ncols) & 1;
-    const int kk = ci / (2 * p.ncols);
-    const int r = n & (g - 1), blk = n >> lg;
-    base[u] = off0 + r + g * (64 * blk + 16 * kk + 8 * h);
-    oo[u] = ci < p.ncols * 4 ? kk * 2 * bblock + (n >> 3) * 256 + h * 128 + (n & 7) * 16 : -1;
-    kks[u] = kk;
-  }
-  auto load = [&](int kp, float (&v)[U][8]) {
-    const int kc = min(2, tm.ksteps - 2 * kp);
+      for (int k = 1; k < 8; ++k) kc += t >= tm.kcoff[k] ? 1 : 0;
+      const int n = t - tm.kcoff[kc];
+      const int i0 = base + (n & (g - 1)) + g * (64 * (n >> lg) + 8 * kc);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i0 = base[u] + 32 * g * kp;
-      if (oo[u] < 0 || kks[u] >= kc) {
+      for (int e = 0; e < 8; ++e) {
+        const int idx = min(i0 + g * e, lim);
+        if constexpr (V == 4) {
+          const float4 w = __ldg(reinterpret_cast<const float4*>(src + idx));
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[u][e] = 0.f;
-      } else if (i0 + 7 * g < lim) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int idx = i0 + g * e;
-          v[u][e] = src[idx + tm.pad * (idx >> sh)];
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int idx = i0 + g * e;
-          v[u][e] = idx < lim ? src[idx + tm.pad * (idx >> sh)] : 0.f;
+          for (int k = 0; k < 4; ++k) {
+            const int j = (k + rot) & 3;
+            v[e][k] = (j & 2) ? ((j & 1) ? w.w : w.z) : ((j & 1) ? w.y : w.x);
+          }
+        } else {
+          const float2 w = __ldg(reinterpret_cast<const float2*>(src + idx));
+          v[e][0] = rot ? w.y : w.x; v[e][1] = rot ? w.x : w.y;
         }
       }
     }
   };
-  float v[U][8];
-  load(0, v);
-  for (int kp = 0; kp < nsp; ++kp, ++qb) {
-    const int kc = min(2, tm.ksteps - 2 * kp);
-    const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
-    TC_TWAIT(&bempty[bs], bph ^ 1, w_be);
-    const long long t_b0 = TC_CLOCK();
-    unsigned char* b0 = bst + (size_t)bs * bstage;
+  auto store = [&](int b, const float (&v)[8][V]) {
+    const int q = tc + kTcsConvThreads * b;
+    if (q < nq) {
+      const int t = q * V;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (oo[u] < 0 || kks[u] >= kc) continue;
-      uint32_t hi[4], lo[4];
+      for (int k = 0; k < V; ++k) {
+        uint32_t hi[4], lo[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) split_bf16x2(v[u][2 * e], v[u][2 * e + 1], hi[e], lo[e]);
-      *reinterpret_cast<uint4*>(b0 + oo[u]) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(b0 + oo[u] + bblock) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        for (int e = 0; e < 4; ++e) split_bf16x2(v[2 * e][k], v[2 * e + 1][k], hi[e], lo[e]);
+        const int r = t + ((k + rot) & (V - 1));                // register slot k holds row (k + rot) % V
+        *reinterpret_cast<uint4*>(buf + (size_t)r * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(buf + (size_t)(brows + r) * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
     }
-    fence_proxy_async_smem();
-    mbar_arrive(&bfull[bs]);
-    if (kp + 1 < nsp) load(kp + 1, v);
-    t_build += TC_CLOCK() - t_b0;
+  };
+  const int nb = (nq + kTcsConvThreads - 1) / kTcsConvThreads;
+  float v[G][8][V];
+#pragma unroll
+  for (int k = 0; k < G; ++k) load(k, v[k]);
+  TC_TWAIT(bempty, par ^ 1, w_be);
+  for (int b0 = 0; b0 < nb; b0 += G) {
+    if (b0 > 0) {
+#pragma unroll
+      for (int k = 0; k < G; ++k) load(b0 + k, v[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < G; ++k) store(b0 + k, v[k]);
+  }
+  fence_proxy_async_smem();
+  mbar_arrive(bfull);
+}
+
+// 32 lanes x 16 consecutive 32-bit TMEM columns -> 16 registers per thread
+__device__ __forceinline__ void tcs_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tcs_wait16(uint32_t (&r)[16], uint32_t (&q)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(q[0]), "+r"(q[1]), "+r"(q[2]), "+r"(q[3]), "+r"(q[4]), "+r"(q[5]), "+r"(q[6]), "+r"(q[7]),
+                 "+r"(q[8]), "+r"(q[9]), "+r"(q[10]), "+r"(q[11]), "+r"(q[12]), "+r"(q[13]), "+r"(q[14]), "+r"(q[15])
+               :: "memory");
+}
+
+// Epilogue of one term for 16 shifts p0 .. p0 + 15 of data row n = blk g + r (TMEM lane n):
+// D = v + w (the hi.hi + lo.hi and hi.lo accumulators, columns (2 p + c)), acc (+)= D (eq. (4):
+// acc = corr_{i+1} + D_i = corr_i), corr_i stores, running peak (lags increase with p: the
+// first maximum wins).
+template <int LG>
+__device__ __forceinline__ void tcs_epi16(const uint32_t (&v)[32], const uint32_t (&w)[32], int n, int p0, bool first,
+                                          float2* acc, float2* cur, PeakF& best) {
+  constexpr int g = 1 << LG;
+  const int tau0 = (n & (g - 1)) + g * (64 * (n >> LG) + p0);
+  const int b = tcs_pad(tau0);
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {                              // 8 shifts at a time: loads, then stores
+    float2 d[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      d[i] = make_float2(__uint_as_float(v[16 * hh + 2 * i]) + __uint_as_float(w[16 * hh + 2 * i]),
+                         __uint_as_float(v[16 * hh + 2 * i + 1]) + __uint_as_float(w[16 * hh + 2 * i + 1]));
+    const int ii = 8 * hh;
+    if (!first) {
+      float2 a[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = acc[b + g * (ii + i) + ((g * (ii + i)) >> 6)];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { d[i].x += a[i].x; d[i].y += a[i].y; }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[b + g * (ii + i) + ((g * (ii + i)) >> 6)] = d[i];
+    if (cur) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) __stcs(cur + tau0 + g * (ii + i), d[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float m2 = mag2f(d[i].x, d[i].y);
+      if (m2 > best.m2) { best.m2 = m2; best.tau = tau0 + g * (ii + i); best.re = d[i].x; best.im = d[i].y; }
+    }
   }
 }
 
@@ -195,51 +295,31 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
   const int S = p.stages;
   uint64_t* afull = reinterpret_cast<uint64_t*>(smem_raw);      // [S]
   uint64_t* aempty = afull + S;                                   // [S]
-  uint64_t* bfull = aempty + S;                                   // [2]
+  uint64_t* bfull = aempty + S;                                   // [2] (one per plane)
   uint64_t* bempty = bfull + 2;                                   // [2]
   uint64_t* dfull = bempty + 2;                                   // [2]
   uint64_t* dempty = dfull + 2;                                   // [2]
-  uint64_t* bandfull = dempty + 2;                                // [2] (one per plane)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bandfull + 2);
-  PeakF* red = reinterpret_cast<PeakF*>(smem_raw + 512);          // [4] epilogue warp partials
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  PeakF* red = reinterpret_cast<PeakF*>(smem_raw + 512);          // [2][8] epilogue warp partials
   unsigned char* ring = smem_raw + L.ring;
-  unsigned char* bst = smem_raw + L.bst;
-  float* stg = reinterpret_cast<float*>(smem_raw + L.stg);
-  float* band = reinterpret_cast<float*>(smem_raw + L.band);      // [2 planes][seg_alloc]
-  float2* acc = reinterpret_cast<float2*>(smem_raw + L.acc);      // [N]
+  unsigned char* bbuf = smem_raw + L.bbuf;
+  float2* acc = reinterpret_cast<float2*>(smem_raw + L.acc);      // [tcs_pad(N) + 2], padded
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nterms = p.J + 1;
-  const int bstage = p.ncols * 128;                               // bytes of one B stage
-  const int bblock = p.ncols * 32;                                // bytes of one (plane, split) block
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bfull[i], 32 * kTcsBuildWarps); mbar_init(&bempty[i], 1);
-      mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * 4);
+      mbar_init(&bfull[i], kTcsConvThreads); mbar_init(&bempty[i], 1);
+      mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kTcsEpiThreads);
     }
-    mbar_init(&bandfull[0], 1);
-    mbar_init(&bandfull[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tslot, 2 * p.ncols_alloc);
+  if (warp == 1) tmem_alloc(tslot, 512);                          // two accumulators of 256 columns
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-
-  // band segment of (row, step) -> smem (two planes), one thread
-  // (pieces of 64 g positions, each followed by `pad` floats, so that the builders' strided
-  //  reads of different 64-lag blocks fall into different banks)
-  auto load_band = [&](long long row, int step, int pl) {
-    const TcsTerm& tm = p.term[step];
-    const float* src = bands + ((size_t)row * (p.J + 1) + tm.band) * 2 * p.stride + tm.a4 + (size_t)pl * p.stride;
-    const int P = 64 << tm.lg;
-    mbar_expect_tx(&bandfull[pl], tm.seg_len * 4u);
-    for (int i = 0, o = 0; o < tm.seg_len; ++i, o += P)
-      bulk_load_g2s(band + pl * p.seg_alloc + i * (P + tm.pad), src + o, (uint32_t)min(P, tm.seg_len - o) * 4u,
-                    &bandfull[pl]);
-  };
 
   if (warp == 0) {
     // ---------------- template operand producer
@@ -266,200 +346,147 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
   } else if (warp == 1) {
     // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform values stay in
     // uniform registers), one elected lane issues the MMAs and the commits
-    {
-      const uint32_t idesc0 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.ncols >> 3) << 17) |
-                              ((uint32_t)(128 >> 4) << 24);
-      const uint32_t idesc2 = (idesc0 & ~(0x3Fu << 17)) | ((uint32_t)((2 * p.ncols) >> 3) << 17);
-      const bool merged = p.merged != 0;
-      uint32_t q = 0, qb = 0, qd = 0;
-      long long w_d = 0, w_af = 0, w_bf = 0;
-      const long long t_start = TC_CLOCK();
-      const uint32_t ring0 = smem_u32(ring), bst0 = smem_u32(bst);
-      // descriptors differ only in their start address: precompute the fixed fields once
-      const uint64_t dA = smem_desc(ring0, 128, 256), dB = smem_desc(bst0, 128, 256);
-      const uint32_t bblock16 = (uint32_t)bblock >> 4, bstage16 = (uint32_t)bstage >> 4;
-      for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
-        for (int step = 0; step < nterms; ++step, ++qd) {
-          const int nsp = tcs_nsp(p.term[step].ksteps);
-          const int ksteps = p.term[step].ksteps;
-          const uint32_t db = qd & 1, dph = (qd >> 1) & 1;
-          TC_TWAIT(&dempty[db], dph ^ 1, w_d);
+    const uint32_t idesc_base = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t idesc256 = idesc_base | ((uint32_t)(256 >> 3) << 17);
+    const uint32_t idesc128 = idesc_base | ((uint32_t)(128 >> 3) << 17);
+    uint32_t q = 0, qt = 0;
+    long long w_d = 0, w_af = 0, w_bf = 0;
+    const long long t_start = TC_CLOCK();
+    const uint32_t ring0 = smem_u32(ring), bbuf0 = smem_u32(bbuf);
+    const uint64_t dT = smem_desc(ring0, 128, 256);              // template: K-major, 8-row groups 256 B apart
+    const uint64_t dD0 = smem_desc(0, 0, 128);                   // data: fixed fields (LBO and start per K step)
+    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+      for (int step = 0; step < nterms; ++step, ++qt) {
+        const TcsTerm& tm = p.term[step];
+        const int ksteps = tm.ksteps, g = 1 << tm.lg;
+        const uint32_t brows16 = (uint32_t)tm.kcoff[8];        // lo block offset in 16-byte units
+        const uint32_t db = qt & 1, dph = (qt >> 1) & 1;
+        TC_TWAIT(&dempty[db], dph ^ 1, w_d);
+        tc_fence_after();
+        const uint32_t dt = tmem + db * 256;
+        for (int pl = 0; pl < 2; ++pl) {
+          TC_TWAIT(&bfull[pl], qt & 1, w_bf);
           tc_fence_after();
-          const uint32_t dt = tmem + db * p.ncols_alloc;
-          for (int st = 0; st < 2 * nsp; ++st, ++q, ++qb) {
-            const int kc = min(2, ksteps - 2 * (st % nsp));
-            const uint32_t slot = q % S, ph = (q / S) & 1;
-            const uint32_t bs = qb & 1, bph = (qb >> 1) & 1;
-            TC_TWAIT(&afull[slot], ph, w_af);
-            TC_TWAIT(&bfull[bs], bph, w_bf);
-            tc_fence_after();
+          const uint32_t b16 = (bbuf0 + (uint32_t)pl * (uint32_t)L.bslot) >> 4;
+          uint32_t slot = 0;
+          for (int ks = 0; ks < ksteps; ++ks) {
+            if ((ks & 1) == 0) {
+              slot = q % S;
+              TC_TWAIT(&afull[slot], (q / S) & 1, w_af);
+              tc_fence_after();
+            }
+            const int i2 = 2 * (ks & 3), X = ks >> 2;
+            const uint32_t row0 = (uint32_t)(tm.kcoff[i2] + X * g);
+            const uint32_t lbo16 = (uint32_t)(tm.kcoff[i2 + 1] - tm.kcoff[i2]);
+            const uint64_t ahi = dD0 | ((uint64_t)lbo16 << 16) | (uint64_t)(b16 + row0);
+            const uint64_t alo = ahi + brows16;
+            const uint64_t thi = dT + (uint64_t)((slot * kTcsAStage + (ks & 1) * (kTcsAStage / 2)) >> 4);
+            const bool last_of_stage = (ks & 1) || ks == ksteps - 1;
             if (elect_one_sync()) {
-              const uint64_t a0 = dA + (uint64_t)(slot * (kTcsAStage >> 4)), b0 = dB + (uint64_t)(bs * bstage16);
-              for (int kk = 0; kk < kc; ++kk) {
-                const uint64_t ahi = a0 + (uint64_t)(kk * (8192 >> 4));
-                const uint64_t alo = ahi + (uint64_t)(4096 >> 4);
-                const uint64_t bhi = b0 + (uint64_t)(kk * 2 * bblock16);
-                const uint32_t acc0 = (st > 0 || kk > 0) ? 1u : 0u;
-                if (merged) {
-                  // D[:, 0:nc] += A_hi B_hi and D[:, nc:2nc] += A_hi B_lo in one MMA over the adjacent
-                  // hi | lo blocks (N = 2 nc, A_hi read once), then D[:, 0:nc] += A_lo B_hi
-                  umma_bf16(dt, ahi, bhi, idesc2, acc0);
-                  umma_bf16(dt, alo, bhi, idesc0, 1u);
-                } else {
-                  const uint64_t blo = bhi + (uint64_t)bblock16;
-                  umma_bf16(dt, ahi, bhi, idesc0, acc0);
-                  umma_bf16(dt, ahi, blo, idesc0, 1u);
-                  umma_bf16(dt, alo, bhi, idesc0, 1u);
-                }
-              }
-              umma_commit(&aempty[slot]);
-              umma_commit(&bempty[bs]);
+              umma_bf16(dt, ahi, thi, idesc256, (pl > 0 || ks > 0) ? 1u : 0u);   // [hi.hi | hi.lo]
+              umma_bf16(dt, alo, thi, idesc128, 1u);                             // + lo.hi
+              if (last_of_stage) umma_commit(&aempty[slot]);
             }
             __syncwarp();
+            if (last_of_stage) ++q;
           }
-          if (elect_one_sync()) umma_commit(&dfull[db]);
+          if (elect_one_sync()) umma_commit(&bempty[pl]);
           __syncwarp();
         }
-      if (p.prof && blockIdx.x == 0 && lane == 0)
-        printf("tcs cta0 mma: total %lld wait dempty %lld afull %lld bfull %lld\n", TC_CLOCK() - t_start, w_d, w_af, w_bf);
-    }
-  } else if (warp < kTcsFirstEpi) {
-    // ---------------- builders (128 threads) + band loader (thread 64)
-    const int tb = threadIdx.x - 32 * kTcsFirstBuild;
-    uint32_t qb = 0, qband = 0;
-    bool first = true;
-    long long w_band = 0, w_be = 0, t_build = 0;
-    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
-      for (int step = 0; step < nterms; ++step, ++qband) {
-        const TcsTerm& tm = p.term[step];
-        if (first && tb == 0) { load_band(row, step, 0); load_band(row, step, 1); }
-        first = false;
-        for (int pl = 0; pl < 2; ++pl) {
-          TC_TWAIT(&bandfull[pl], qband & 1, w_band);
-          const float* src = band + pl * p.seg_alloc;
-          switch (tm.lg) {
-            case 1: tcs_build_phase<1>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
-            case 2: tcs_build_phase<2>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
-            case 3: tcs_build_phase<3>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
-            case 4: tcs_build_phase<4>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
-            case 5: tcs_build_phase<5>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
-            case 6: tcs_build_phase<6>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
-            default: tcs_build_phase<-1>(p, tm, tb, src, bst, bfull, bempty, qb, w_be, t_build); break;
-          }
-          // every builder is done with this plane's segment: load the next term's (overlaps the
-          // other plane's stages)
-          named_bar(1, 32 * kTcsBuildWarps);
-          if (tb == 0) {
-            long long nrow = row;
-            int nstep = step + 1;
-            if (nstep == nterms) { nstep = 0; nrow += gridDim.x; }
-            if (nrow < p.rows) load_band(nrow, nstep, pl);
-          }
-        }
+        if (elect_one_sync()) umma_commit(&dfull[db]);
+        __syncwarp();
       }
-    if (p.prof && blockIdx.x == 0 && tb == 0)
-      printf("tcs cta0 builder: wait band %lld bempty %lld build %lld\n", w_band, w_be, t_build);
+    if (p.prof && blockIdx.x == 0 && lane == 0)
+      printf("tcs cta0 mma: total %lld wait dempty %lld afull %lld bfull %lld\n", TC_CLOCK() - t_start, w_d, w_af, w_bf);
+  } else if (warp < kTcsFirstEpi) {
+    // ---------------- converters: warps 2-4 the re plane, 5-7 the im plane
+    const int pl = (warp - kTcsFirstConv) / 3;
+    const int tc = threadIdx.x - 32 * kTcsFirstConv - kTcsConvThreads * pl;
+    unsigned char* buf = bbuf + (size_t)pl * L.bslot;
+    uint32_t qt = 0;
+    long long w_be = 0;
+    for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
+      for (int step = 0; step < nterms; ++step, ++qt) {
+        const TcsTerm& tm = p.term[step];
+        const float* src = bands + (((size_t)row * (p.J + 1) + tm.band) * 2 + pl) * p.stride;
+        if (tm.lg >= 2) tcs_convert<4>(p, tm, tc, src, buf, &bfull[pl], &bempty[pl], qt & 1, w_be);
+        else tcs_convert<2>(p, tm, tc, src, buf, &bfull[pl], &bempty[pl], qt & 1, w_be);
+      }
+    if (p.prof && blockIdx.x == 0 && tc == 0) printf("tcs cta0 converter %d: wait bempty %lld\n", pl, w_be);
   } else {
-    // ---------------- epilogue (128 threads, TMEM lane quarter = warp % 4)
+    // ---------------- epilogue (256 threads): TMEM lane quarter = warp % 4 (data rows n),
+    // half h = shifts p in [32 h, 32 h + 32)
     const int te = threadIdx.x - 32 * kTcsFirstEpi;
-    const int quarter = warp & 3;
-    const int m = 32 * quarter + lane;                            // TMEM lane = A row (64 c + p)
-    uint32_t qd = 0;
-    long long w_df = 0, t_epi = 0;
+    const int quarter = warp & 3, h = (warp - kTcsFirstEpi) >> 2;
+    const int n = 32 * quarter + lane;                            // TMEM lane = data row
+    const bool live = n < p.ncols;
+    uint32_t qt = 0;
+    long long w_df = 0, t_epi = 0, t_b = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      for (int step = 0; step < nterms; ++step, ++qd) {
+      for (int step = 0; step < nterms; ++step, ++qt) {
         const TcsTerm& tm = p.term[step];
         const int ti = p.J - step;
-        const int g = 1 << tm.lg;
-        const uint32_t db = qd & 1, dph = (qd >> 1) & 1;
+        const uint32_t db = qt & 1, dph = (qt >> 1) & 1;
         float2* cur = p.want_corr ? corr + ((size_t)row * (p.J + 1) + ti) * p.N : nullptr;
-        PeakF best; best.m2 = 0.f; best.tau = -1; best.re = 0.f; best.im = 0.f;
+        const bool first = step == 0;
         TC_TWAIT(&dfull[db], dph, w_df);
         const long long t_e0 = TC_CLOCK();
         tc_fence_after();
-        const int lgR = tm.lg < 5 ? tm.lg : 5;
-        const int R = 1 << lgR;                                   // residues per chunk
-        const int nch = (p.ncols + 31) / 32;
-        const int cw = p.ncols < 32 ? p.ncols : 32;               // columns per chunk
-        for (int ch = 0; ch < nch; ++ch) {
-          const int n0 = ch * 32;
-          uint32_t v[32];
-          const uint32_t ta = tmem + db * p.ncols_alloc + ((uint32_t)(32 * quarter) << 16) + n0;
+        PeakF best; best.m2 = -1.f; best.tau = 0; best.re = 0.f; best.im = 0.f;
+#pragma unroll 1
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const int p0 = 32 * h + 16 * s2;
+          const uint32_t ta = tmem + db * 256 + ((uint32_t)(32 * quarter) << 16) + 2 * p0;
+          uint32_t v[32], w[32];
           tmem_ld32_nowait(ta, v);
+          tmem_ld32_nowait(ta + 128, w);
           tmem_wait_ld(v);
-          if (p.merged) {                                         // add the A_hi B_lo half
-            uint32_t w[32];
-            tmem_ld32_nowait(ta + p.ncols, w);
-            tmem_wait_ld(w);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(w[i]));
-          }
-          if (ch == nch - 1) { tc_fence_before(); mbar_arrive(&dempty[db]); }
-          // staging: row m, 32 floats, 16-byte chunks XOR-swizzled by m % 8
-#pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4)
-            *reinterpret_cast<uint4*>(stg + m * 32 + ((c4 ^ (m & 7)) << 2)) = make_uint4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
-          if (ch == 0 && te == 0) bulk_wait_read_all();            // corr_{i+1} store has read acc
-          named_bar(2, 128);
-          // outputs of the chunk in lag order: idx -> (bl, p, rr); n_local = bl R + rr
-          const int r0 = n0 & (g - 1), blk0 = n0 >> tm.lg;
-          // acc[tau] (+)= D: lanes take consecutive lags
-          const int nper = (64 * cw) / 128;
-#pragma unroll 4
-          for (int i = 0; i < nper; ++i) {
-            const int idx = te + 128 * i;
-            const int rr = idx & (R - 1);
-            const int pp = (idx >> lgR) & 63;
-            const int bl = idx >> (lgR + 6);
-            const int nl = (bl << lgR) + rr;
-            const int tau = r0 + rr + g * (64 * (blk0 + bl) + pp);
-            const int cre = ((nl >> 2) ^ (pp & 7)) << 2;
-            float re = stg[pp * 32 + cre + (nl & 3)];
-            float im = stg[(64 + pp) * 32 + cre + (nl & 3)];
-            if (step > 0) {
-              const float2 a = acc[tau];
-              re += a.x; im += a.y;
-            }
-            acc[tau] = make_float2(re, im);
-            const float m2 = mag2f(re, im);
-            if (best.tau < 0 || m2 > best.m2 || (m2 == best.m2 && tau < best.tau)) {
-              best.m2 = m2; best.tau = tau; best.re = re; best.im = im;
+          tmem_wait_ld(w);
+          if (s2 == 1) { tc_fence_before(); mbar_arrive(&dempty[db]); }   // this thread's TMEM reads are done
+          if (live) {
+            switch (tm.lg) {
+              case 1: tcs_epi16<1>(v, w, n, p0, first, acc, cur, best); break;
+              case 2: tcs_epi16<2>(v, w, n, p0, first, acc, cur, best); break;
+              case 3: tcs_epi16<3>(v, w, n, p0, first, acc, cur, best); break;
+              case 4: tcs_epi16<4>(v, w, n, p0, first, acc, cur, best); break;
+              case 5: tcs_epi16<5>(v, w, n, p0, first, acc, cur, best); break;
+              case 6: tcs_epi16<6>(v, w, n, p0, first, acc, cur, best); break;
+              default: tcs_epi16<7>(v, w, n, p0, first, acc, cur, best); break;
             }
           }
-          named_bar(2, 128);
         }
-        // the row's peak at this scale: warp argmax (largest |.|^2, then smallest lag), then 4 warps
-        const unsigned mb = best.tau >= 0 ? __float_as_uint(best.m2) : 0u;
+        // warp argmax (largest |.|^2, then smallest lag), then the 8 warps (red double-buffered
+        // by term parity: te 0 reads it after the barrier, the next term writes the other half)
+        const unsigned mb = best.m2 >= 0.f ? __float_as_uint(best.m2) : 0u;   // m2 >= 0: bit order = value order
         const unsigned mmax = __reduce_max_sync(0xffffffffu, mb);
-        const unsigned cand = (best.tau >= 0 && mb == mmax) ? (unsigned)best.tau : 0xffffffffu;
-        const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
-        if (best.tau >= 0 && (unsigned)best.tau == tmin) red[warp - kTcsFirstEpi] = best;
-        fence_proxy_async_smem();                                  // acc writes -> visible to the bulk copy
-        named_bar(2, 128);
-        if (te == 0 && cur) {
-          bulk_store_s2g(cur, acc, (uint32_t)p.N * 8u);
-          bulk_commit();
-        }
+        const unsigned tmin = __reduce_min_sync(0xffffffffu, (best.m2 >= 0.f && mb == mmax) ? (unsigned)best.tau : 0xffffffffu);
+        PeakF* rd = red + (qt & 1) * kTcsEpiWarps;
+        if (lane == 0) rd[warp - kTcsFirstEpi].tau = -1;
+        __syncwarp();
+        if (best.m2 >= 0.f && mb == mmax && (unsigned)best.tau == tmin) rd[warp - kTcsFirstEpi] = best;
+        const long long t_c = TC_CLOCK();
+        // every lag of corr_i is in acc before the next term adds to it; the partials are complete
+        named_bar(2, kTcsEpiThreads);
+        t_b += TC_CLOCK() - t_c;
         if (te == 0 && lag) {
-          PeakF b = red[0];
-          for (int w = 1; w < 4; ++w) {
-            const PeakF o = red[w];
-            if (o.m2 > b.m2 || (o.m2 == b.m2 && o.tau < b.tau)) b = o;
+          PeakF b; b.tau = -1; b.m2 = 0.f; b.re = 0.f; b.im = 0.f;
+          for (int w2 = 0; w2 < kTcsEpiWarps; ++w2) {
+            const PeakF o = rd[w2];
+            if (o.tau >= 0 && (b.tau < 0 || o.m2 > b.m2 || (o.m2 == b.m2 && o.tau < b.tau))) b = o;
           }
           const size_t e = (size_t)row * (p.J + 1) + ti;
           lag[e] = b.tau;
           if (val) val[e] = make_float2(b.re, b.im);
         }
-        named_bar(2, 128);
         t_epi += TC_CLOCK() - t_e0;
       }
     }
-    if (te == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-    if (p.prof && blockIdx.x == 0 && te == 0) printf("tcs cta0 epilogue: wait dfull %lld work %lld\n", w_df, t_epi);
+    if (p.prof && blockIdx.x == 0 && te == 0)
+      printf("tcs cta0 epilogue: wait dfull %lld work %lld (barrier %lld)\n", w_df, t_epi, t_b);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 2 * p.ncols_alloc);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace sidwt

@@ -237,7 +237,7 @@ static void configure(sidwt_plan_s* p) {
   } else {
     ML = std::max(ML, 1 << J);
   }
-  if (is_int(p)) ML = (int)rup(ML, 4);      // int8 tensor-core path: 16-byte aligned band segments
+  ML = (int)rup(ML, 4);      // 16-byte aligned band segments (int8 and single-template tensor-core paths)
   if (p->ext == SIDWT_EXT_PERIODIC) { ML = 0; MR = 0; }
   p->ML = ML; p->MR = MR;
   p->stride = rup(ML + p->N + MR, 32);
@@ -374,7 +374,7 @@ static void configure_tc(sidwt_plan_s* p) {
 }
 
 // Single-template tensor-core path (corr_tcs.cuh): float families, one template,
-// symmetric extension, N / 64 columns in [16, 256] (multiple of 16), every residue class
+// symmetric extension, N / 64 columns in [16, 128] (multiple of 16), every residue class
 // at least one 64-lag block long (2^J <= N / 64).  SIDWT_TCS=0 disables it.
 static void configure_tcs(sidwt_plan_s* p) {
   p->tcs = false;
@@ -386,16 +386,13 @@ static void configure_tcs(sidwt_plan_s* p) {
   if (p->paper || is_int(p) || p->n_t != 1 || p->ext != SIDWT_EXT_SYMMETRIC || p->tc) return;
   if (p->N % 64 != 0) return;
   const int ncols = (int)(p->N / 64);
-  if (ncols < 16 || ncols > 128 || ncols % 16 != 0 || (1LL << p->J) > ncols) return;   // builders: 2 chunks/thread
+  if (ncols < 16 || ncols > 128 || ncols % 16 != 0 || (1LL << p->J) > ncols) return;
   TcsParams& t = p->tcsp;
   t = TcsParams{};
   t.N = (int)p->N; t.J = p->J; t.stride = (int)p->stride; t.ML = p->ML; t.ncols = ncols;
-  // merged hi | lo products need 2 ncols TMEM columns per accumulator (double-buffered: <= 512)
-  t.merged = ncols <= 128 ? 1 : 0;
-  if (const char* e = std::getenv("SIDWT_TCS_MERGED")) t.merged = atoi(e) != 0 && ncols <= 128;
-  t.ncols_alloc = 32;
-  while (t.ncols_alloc < (t.merged ? 2 : 1) * ncols) t.ncols_alloc *= 2;
-  int kofs = 0, seg = 0;
+  t.ncols_alloc = 32;                                             // one accumulator, double-buffered
+  while (t.ncols_alloc < ncols) t.ncols_alloc *= 2;
+  int kofs = 0;
   for (int step = 0; step <= p->J; ++step) {
     const int ti = p->J - step;
     TcsTerm& tm = t.term[step];
@@ -404,21 +401,14 @@ static void configure_tcs(sidwt_plan_s* p) {
     tm.ksteps = (int)cdiv(tm.ntap + 63, 16);
     tm.kofs = kofs; kofs += tm.ksteps;
     const int g = 1 << tm.lg;
-    tm.pos_lo = g * tm.kmin;
-    const int64_t pos_hi = p->N + (int64_t)g * (tm.kmin + 16 * tm.ksteps - 64);   // one past the last position read
-    const int64_t a = tm.pos_lo + p->ML;
+    const int64_t a = (int64_t)p->ML + (int64_t)g * tm.kmin;   // band index of (r = 0, m = 0)
     if (a < 0) return;
-    tm.a4 = (int)(a & ~3LL);
-    const int64_t end = std::min<int64_t>(pos_hi + p->ML, p->stride);
-    tm.seg_len = (int)rup(end - tm.a4, 4);
-    tm.pad = (g >= 4 && g <= 32) ? g : 4;
-    const int64_t span = rup(pos_hi + p->ML - tm.a4, 4);        // segment indices the builders touch
-    seg = std::max<int>(seg, (int)(span + tm.pad * cdiv(span, (int64_t)64 * g)));
+    tcs_term_rows(tm, ncols);
+    t.brows_max = std::max(t.brows_max, tm.kcoff[8]);
   }
-  t.seg_alloc = seg;
   p->tcs_total_ksteps = kofs;
-  t.stages = 4;
-  if (const char* e = std::getenv("SIDWT_TCS_STAGES")) t.stages = std::max(2, std::min(6, atoi(e)));
+  t.stages = 6;
+  if (const char* e = std::getenv("SIDWT_TCS_STAGES")) t.stages = std::max(2, std::min(8, atoi(e)));
   while (t.stages > 2 && tcs_smem_layout(t).total > 227 * 1024) --t.stages;
   if (tcs_smem_layout(t).total > 227 * 1024) return;
   p->tcs_smem = tcs_smem_layout(t).total;
@@ -590,7 +580,7 @@ sidwt_status sidwt_template_load(sidwt_plan p, const void* host_templates, int64
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       if (p->d_tcs_img) { cudaFree(p->d_tcs_img); p->d_tcs_img = nullptr; }
-      cudaFree(p->d_taps); p->d_taps = nullptr;
+          cudaFree(p->d_taps); p->d_taps = nullptr;
       return cuda_status(e);
     }
   }
