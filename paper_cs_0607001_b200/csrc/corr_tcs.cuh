@@ -61,6 +61,7 @@ struct TcsTerm {
   int band, lg, kmin, ntap, toff;
   int ksteps, kofs;                             // K steps (16 taps each) and first K step in the image
   int kcoff[9];                                 // first buffer row of chunk plane kc (kcoff[8] = rows per split)
+  int pf_a4, pf_len;                            // band floats [pf_a4, pf_a4 + pf_len) the converters read (L2 prefetch)
 };
 
 struct TcsParams {
@@ -133,6 +134,10 @@ __global__ void k_tcs_images(const float2* __restrict__ taps, TcsParams p, int t
     const __nv_bfloat16 o = __float2bfloat16_rn(split == 0 ? hi : lo);
     *reinterpret_cast<__nv_bfloat16*>(blk + (m >> 3) * 256 + (kk >> 3) * 128 + (m & 7) * 16 + (kk & 7) * 2) = o;
   }
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" :: "l"(g), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ bool elect_one_sync() {
@@ -330,6 +335,17 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
         for (int step = 0; step < nterms; ++step) {
           const TcsTerm& tm = p.term[step];
           const int nsp = tcs_nsp(tm.ksteps);
+          {                                                       // the band segments two terms ahead -> L2
+            long long nrow = row;
+            int nstep = step + 2;
+            if (nstep >= nterms) { nstep -= nterms; nrow += gridDim.x; }
+            if (nrow < p.rows) {
+              const TcsTerm& tn = p.term[nstep];
+              const float* b0 = bands + ((size_t)nrow * (p.J + 1) + tn.band) * 2 * p.stride + tn.pf_a4;
+              prefetch_l2(b0, (uint32_t)tn.pf_len * 4u);
+              prefetch_l2(b0 + p.stride, (uint32_t)tn.pf_len * 4u);
+            }
+          }
           for (int st = 0; st < 2 * nsp; ++st, ++q) {
             const int pl = st / nsp, k0 = 2 * (st % nsp), kc = min(2, tm.ksteps - k0);
             const uint32_t slot = q % S, ph = (q / S) & 1;

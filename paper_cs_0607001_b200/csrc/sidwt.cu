@@ -405,6 +405,13 @@ static void configure_tcs(sidwt_plan_s* p) {
     if (a < 0) return;
     tcs_term_rows(tm, ncols);
     t.brows_max = std::max(t.brows_max, tm.kcoff[8]);
+    int64_t imax = 0;                                              // last band index any buffer row reads
+    for (int kc = 0; kc < 8; ++kc) {
+      const int W = tm.kcoff[kc + 1] - tm.kcoff[kc];
+      if (W > 0) imax = std::max<int64_t>(imax, a + (g - 1) + (int64_t)g * (64 * ((W - 1) >> tm.lg) + 8 * kc + 7));
+    }
+    tm.pf_a4 = (int)(a & ~3LL);
+    tm.pf_len = (int)rup(std::min<int64_t>(imax + 1, p->stride) - tm.pf_a4, 4);
   }
   p->tcs_total_ksteps = kofs;
   t.stages = 6;
