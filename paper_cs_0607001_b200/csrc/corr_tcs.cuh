@@ -29,8 +29,8 @@
 // planes 2 i and 2 i + 1.  Converter warps fill the buffer once per (term, plane) with
 // coalesced loads of the fine-grid band from global memory (a permutation of the
 // band segment, no duplication), split into hi / lo bf16; the MMA then runs all K steps
-// of the plane from it.  Two buffers (one per plane) let a plane of the next term be
-// converted while the other is multiplied.
+// of the plane from it.  Three buffers (term-plane s in buffer s % 3) let the converters run
+// up to two term-planes ahead of the MMAs.
 //
 // Eq. (4) and the peaks in one epilogue pass.  TMEM lane n holds the
 // data row (blk, r): 64 consecutive lags of residue class r, re and im side by side.  One
@@ -55,6 +55,7 @@ constexpr int kTcsThreads = 32 * kTcsWarps;
 constexpr int kTcsFirstConv = 2, kTcsConvWarps = 6;     // 3 warps (96 threads) per plane
 constexpr int kTcsConvThreads = 96;
 constexpr int kTcsFirstEpi = 8, kTcsEpiWarps = 8, kTcsEpiThreads = 32 * kTcsEpiWarps;
+constexpr int kTcsSlots = 3;                     // data-operand buffers (term-plane s uses slot s % 3)
 constexpr int kTcsAStage = 16384;               // one K step: 2 planes x (hi, lo) x 128 rows x 16 x bf16
 
 struct TcsTerm {
@@ -100,7 +101,7 @@ __host__ __device__ inline TcsSmem tcs_smem_layout(const TcsParams& p) {
   L.ring = 1024;
   L.bbuf = L.ring + (size_t)p.stages * kTcsAStage;
   L.bslot = (size_t)2 * p.brows_max * 16;         // one plane: (hi, lo) x rows x 16 B
-  L.acc = L.bbuf + 2 * L.bslot;
+  L.acc = L.bbuf + kTcsSlots * L.bslot;
   L.total = L.acc + (size_t)(tcs_pad(p.N) + 2) * 8;   // the row's running corr (eq. (4) suffix sum), float2
   return L;
 }
@@ -300,9 +301,9 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
   const int S = p.stages;
   uint64_t* afull = reinterpret_cast<uint64_t*>(smem_raw);      // [S]
   uint64_t* aempty = afull + S;                                   // [S]
-  uint64_t* bfull = aempty + S;                                   // [2] (one per plane)
-  uint64_t* bempty = bfull + 2;                                   // [2]
-  uint64_t* dfull = bempty + 2;                                   // [2]
+  uint64_t* bfull = aempty + S;                                   // [kTcsSlots]
+  uint64_t* bempty = bfull + kTcsSlots;                           // [kTcsSlots]
+  uint64_t* dfull = bempty + kTcsSlots;                           // [2]
   uint64_t* dempty = dfull + 2;                                   // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
   PeakF* red = reinterpret_cast<PeakF*>(smem_raw + 512);          // [2][8] epilogue warp partials
@@ -314,10 +315,8 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bfull[i], kTcsConvThreads); mbar_init(&bempty[i], 1);
-      mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kTcsEpiThreads);
-    }
+    for (int i = 0; i < kTcsSlots; ++i) { mbar_init(&bfull[i], kTcsConvThreads); mbar_init(&bempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kTcsEpiThreads); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tslot, 512);                          // two accumulators of 256 columns
@@ -381,9 +380,10 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
         tc_fence_after();
         const uint32_t dt = tmem + db * 256;
         for (int pl = 0; pl < 2; ++pl) {
-          TC_TWAIT(&bfull[pl], qt & 1, w_bf);
+          const uint32_t sidx = 2 * qt + pl, bs = sidx % kTcsSlots;       // term-plane sidx, its buffer
+          TC_TWAIT(&bfull[bs], (sidx / kTcsSlots) & 1, w_bf);
           tc_fence_after();
-          const uint32_t b16 = (bbuf0 + (uint32_t)pl * (uint32_t)L.bslot) >> 4;
+          const uint32_t b16 = (bbuf0 + bs * (uint32_t)L.bslot) >> 4;
           uint32_t slot = 0;
           for (int ks = 0; ks < ksteps; ++ks) {
             if ((ks & 1) == 0) {
@@ -406,7 +406,7 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
             __syncwarp();
             if (last_of_stage) ++q;
           }
-          if (elect_one_sync()) umma_commit(&bempty[pl]);
+          if (elect_one_sync()) umma_commit(&bempty[bs]);
           __syncwarp();
         }
         if (elect_one_sync()) umma_commit(&dfull[db]);
@@ -418,15 +418,17 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
     // ---------------- converters: warps 2-4 the re plane, 5-7 the im plane
     const int pl = (warp - kTcsFirstConv) / 3;
     const int tc = threadIdx.x - 32 * kTcsFirstConv - kTcsConvThreads * pl;
-    unsigned char* buf = bbuf + (size_t)pl * L.bslot;
     uint32_t qt = 0;
     long long w_be = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x)
       for (int step = 0; step < nterms; ++step, ++qt) {
         const TcsTerm& tm = p.term[step];
         const float* src = bands + (((size_t)row * (p.J + 1) + tm.band) * 2 + pl) * p.stride;
-        if (tm.lg >= 2) tcs_convert<4>(p, tm, tc, src, buf, &bfull[pl], &bempty[pl], qt & 1, w_be);
-        else tcs_convert<2>(p, tm, tc, src, buf, &bfull[pl], &bempty[pl], qt & 1, w_be);
+        const uint32_t sidx = 2 * qt + pl, bs = sidx % kTcsSlots;         // term-plane sidx, its buffer
+        unsigned char* buf = bbuf + (size_t)bs * L.bslot;
+        const uint32_t par = (sidx / kTcsSlots) & 1;
+        if (tm.lg >= 2) tcs_convert<4>(p, tm, tc, src, buf, &bfull[bs], &bempty[bs], par, w_be);
+        else tcs_convert<2>(p, tm, tc, src, buf, &bfull[bs], &bempty[bs], par, w_be);
       }
     if (p.prof && blockIdx.x == 0 && tc == 0) printf("tcs cta0 converter %d: wait bempty %lld\n", pl, w_be);
   } else {
