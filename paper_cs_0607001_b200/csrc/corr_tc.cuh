@@ -585,7 +585,7 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
     unsigned char* epi = smem_raw + L.epi + ew * kTcEpiBytes;
     const int ta = lane & 3, tb = lane >> 2;
     const int tr0 = (tb >> 1) + 4 * (tb & 1), tr1 = 8 + tr0;     // template rows (of the warp's 16)
-    long long w_acc = 0, t_start = TC_CLOCK();
+    long long w_acc = 0, t_start = TC_CLOCK(), w_tm = 0, w_rd = 0, t_st = 0, t_pk = 0;
     long long u = 0;
     int cb = 0;                                                 // staging buffer of the next chunk
     for (int pair = blockIdx.x; pair < (int)p.npairs; pair += gridDim.x) {
@@ -600,12 +600,22 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
         float bm2[2] = {-1.f, -1.f}, bre[2] = {0.f, 0.f}, bim[2] = {0.f, 0.f};
         int btau[2] = {0x7fffffff, 0x7fffffff};
         const uint32_t tcol = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(a * 256 + hh * 128);
-#pragma unroll 1
+        // TMEM loads double-buffered: chunk c + 1 is in flight while chunk c is staged and scanned
+        uint32_t va[32], vb[32];
+        tmem_ld16x256_x4(tcol, va, 0);
+        tmem_ld16x256_x4(tcol + (16u << 16), va, 16);
+#pragma unroll
         for (int c = 0; c < 4; ++c, cb ^= 1) {
-          uint32_t v[32];
-          tmem_ld16x256_x4(tcol + c * 32, v, 0);
-          tmem_ld16x256_x4(tcol + (16u << 16) + c * 32, v, 16);
+          uint32_t (&v)[32] = (c & 1) ? vb : va;
+          uint32_t (&vn)[32] = (c & 1) ? va : vb;
+          const long long c0 = TC_CLOCK();
           tmem_wait_ld(v);
+          const long long c1 = TC_CLOCK();
+          w_tm += c1 - c0;
+          if (c < 3) {
+            tmem_ld16x256_x4(tcol + (c + 1) * 32, vn, 0);
+            tmem_ld16x256_x4(tcol + (16u << 16) + (c + 1) * 32, vn, 16);
+          }
           if (c == 3) {                                         // accumulator fully read: release it
             tc_fence_before();
             __syncwarp();
@@ -613,8 +623,11 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
           }
           unsigned char* buf = epi + cb * 4096;
           const int tau_c = tau_h + c * 32;
+          const long long c2 = TC_CLOCK();
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");   // buffer cb free
           __syncwarp();
+          const long long c3 = TC_CLOCK();
+          w_rd += c3 - c2;
 #pragma unroll
           for (int kb = 0; kb < 2; ++kb) {
             const int r = kb ? tr1 : tr0;
@@ -640,6 +653,8 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
             }
             bulk_commit();                                      // (possibly empty) group per chunk
           }
+          const long long c4 = TC_CLOCK();
+          t_st += c4 - c3;
           if (p.want_peaks) {
 #pragma unroll
             for (int kb = 0; kb < 2; ++kb) {
@@ -666,6 +681,7 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
               }
             }
           }
+          t_pk += TC_CLOCK() - c4;
         }
         if (p.want_peaks) {
 #pragma unroll
@@ -691,7 +707,8 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
     if (lane == 0) bulk_wait_all();
     __syncwarp();
     if (p.prof && blockIdx.x == 0 && lane == 0)
-      printf("[tc prof] epilogue warp %d: total %lld  wait_accfull %lld\n", warp, TC_CLOCK() - t_start, w_acc);
+      printf("[tc prof] epilogue warp %d: total %lld  wait_accfull %lld tmem %lld stgread %lld stage %lld peak %lld\n", warp,
+             TC_CLOCK() - t_start, w_acc, w_tm, w_rd, t_st, t_pk);
   }
   tc_fence_before();
   __syncthreads();
