@@ -61,6 +61,9 @@ EDGE = [
     (2, 5, 4096, 130),
     (2, 3, 8192, 33),
     (1, 2, 8192, 1000),
+    (1, 7, 8192, 600),      # g = 2^7 = N / 64: residue blocks of one 64-lag block, the lg = 7 epilogue
+    (0, 5, 2048, 200),      # N / 64 = 32 data rows (the M = 128 MMA rows past them are ignored)
+    (2, 4, 1024, 100),      # the smallest tile: N / 64 = 16 data rows
 ]
 
 
