@@ -235,24 +235,6 @@ __device__ __forceinline__ void tcs_convert(const TcsParams& p, const TcsTerm& t
   mbar_arrive(bfull);
 }
 
-// 32 lanes x 16 consecutive 32-bit TMEM columns -> 16 registers per thread
-__device__ __forceinline__ void tcs_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tcs_wait16(uint32_t (&r)[16], uint32_t (&q)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
-                 "+r"(q[0]), "+r"(q[1]), "+r"(q[2]), "+r"(q[3]), "+r"(q[4]), "+r"(q[5]), "+r"(q[6]), "+r"(q[7]),
-                 "+r"(q[8]), "+r"(q[9]), "+r"(q[10]), "+r"(q[11]), "+r"(q[12]), "+r"(q[13]), "+r"(q[14]), "+r"(q[15])
-               :: "memory");
-}
-
 // Epilogue of one term for 16 shifts p0 .. p0 + 15 of data row n = blk g + r (TMEM lane n):
 // D = v + w (the hi.hi + lo.hi and hi.lo accumulators, columns (2 p + c)), acc (+)= D (eq. (4):
 // acc = corr_{i+1} + D_i = corr_i), corr_i stores, running peak (lags increase with p: the
