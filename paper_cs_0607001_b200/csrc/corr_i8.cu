@@ -36,10 +36,12 @@
 // HBM (128 contiguous bytes per thread) and the row's peak per scale (a7) is reduced in the
 // epilogue -- no partials, no finalize kernel.
 //
-// Roles (448 threads): warp 0 bulk-copy loader (band segments of both components, B images);
-// warp 1 MMA issuer (whole warp, one elected lane issues); warps 2-5 builders (int32 band segment
-// -> byte-digit planes, range flag); warps 6-13 epilogue, two per TMEM lane quarter (warp % 4),
-// each eight of the 16 shifts of a lag block; corr leaves through swizzled staging and TMA stores.
+// Roles (512 threads, whole warpgroups so that setmaxnreg can move registers to the epilogue):
+// warp 0 bulk-copy loader (band segments of both components, B images); warps 1, 2 MMA issuers
+// (whole warp, one elected lane issues; one tile each); warp 3 idle; warps 4-7 builders (int32
+// band segment -> byte-digit planes, range flag); warps 8-15 epilogue, two per TMEM lane quarter
+// (warp % 4), each eight of the 16 shifts of a lag block; corr leaves through swizzled staging
+// and TMA stores.
 #define SIDWT_NO_KERNELS
 #include "kernels.cuh"
 #include "corr_tc.cuh"
@@ -55,22 +57,32 @@ namespace sidwt {
 // epilogue: kI8HW warps per TMEM lane quarter, each kI8PL of the 16 shifts of every lag block
 constexpr int kI8HW = 2, kI8PL = 16 / kI8HW;     // measured: 4 warps per quarter issue-bound (C5 corr 9.05 vs 8.38 ms)
 static_assert(kI8HW == 2, "accumulator column order n = 32 a + 16 (p / 8) + 8 oc + p % 8 assumes two halves");
-constexpr int kI8FirstBuild = 2, kI8BuildWarps = 4, kI8FirstEpi = 6, kI8EpiWarps = 4 * kI8HW;
-constexpr int kI8Mma2 = kI8FirstEpi + kI8EpiWarps;      // second MMA-issuing warp
-constexpr int kI8Warps = kI8Mma2 + 1;
+// roles by warpgroup (setmaxnreg moves registers between warpgroups): warps 0-3 loader, two MMA
+// issuers and one idle warp; warps 4-7 builders; warps 8-15 epilogue
+constexpr int kI8FirstBuild = 4, kI8BuildWarps = 4, kI8FirstEpi = 8, kI8EpiWarps = 4 * kI8HW;
+constexpr int kI8Mma2 = 2;                               // second MMA-issuing warp
+constexpr int kI8Warps = kI8FirstEpi + kI8EpiWarps;
+constexpr int kI8RegsCtl = 56, kI8RegsBuild = 72, kI8RegsEpi = 192;   // per thread, after setmaxnreg
+static_assert(kI8FirstBuild % 4 == 0 && kI8FirstEpi % 4 == 0 && kI8Warps % 4 == 0, "roles are whole warpgroups");
+static_assert(kI8FirstBuild * kI8RegsCtl + kI8BuildWarps * kI8RegsBuild + kI8EpiWarps * kI8RegsEpi <= 2048,
+              "register budget: 64 K registers per SM");
 constexpr int kI8Threads = 32 * kI8Warps;
 constexpr int kI8BuildThreads = 32 * kI8BuildWarps;
 // TMEM: 512 columns, two accumulator buffers of 256 (tile t+1's MMAs overlap tile t's epilogue)
 // when dmax * ncol <= 256, else one buffer of 512
 constexpr int kI8TmemCols = 512;
 
-struct I8Smem { size_t red, stg, band, stream, img, total; };
+struct I8Smem { size_t red, cand, cmeta, wscr, stg, band, stream, img, total; };
 constexpr int kI8RowBytes = 8 * kI8PL;             // one lane's corr slice: kI8PL lags x 8 B (32, 64 or 128: TMA swizzle span)
 constexpr int kI8StgBytes = 32 * kI8RowBytes;       // per epilogue warp and buffer: 32 lag blocks
 __host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
   I8Smem L;
-  L.red = 1024;                                                         // [2 rows][J+1][kI8EpiWarps] peak partials
-  L.stg = (L.red + (size_t)2 * kI8MaxTerms * kI8EpiWarps * 24 + 1023) & ~(size_t)1023;   // swizzled TMA staging
+  const size_t nterms = (size_t)p.J + 1;
+  L.red = 1024;                                                         // [2 rows][J+1][kI8EpiWarps] warp peak candidates
+  L.cand = L.red + 2 * nterms * kI8EpiWarps * 24;                       // [2 rows][J+1][16 lags] int2: the key holder's corr values
+  L.cmeta = L.cand + 2 * nterms * 16 * 8;                               // [2 rows][J+1] (taken, first lag)
+  L.wscr = (L.cmeta + 2 * nterms * 8 + 15) & ~(size_t)15;               // [kI8EpiWarps][16 lags] int2: scratch of the rare tie path
+  L.stg = (L.wscr + (size_t)kI8EpiWarps * 16 * 8 + 1023) & ~(size_t)1023;   // swizzled TMA staging
   L.band = L.stg + (size_t)kI8EpiWarps * 2 * kI8StgBytes;
   L.stream = (L.band + (size_t)p.nband * 2 * p.seg_alloc * 4 + 127) & ~(size_t)127;
   L.img = L.stream + (size_t)p.nstream * 2 * p.dmax * p.plane;
@@ -234,10 +246,15 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   uint64_t* imgempty = imgfull + 4;                                   // [NI]
   uint64_t* dfull = imgempty + 4;                                     // [2]
   uint64_t* dempty = dfull + 2;                                       // [2]
+  uint64_t* hkey = dempty + 2;                                        // peak keys of a term posted (one arrival per epilogue warp)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + 256);
   int* dcnt = reinterpret_cast<int*>(smem_raw + 264);                 // [2] digits used per TMEM buffer
   int* sflag = reinterpret_cast<int*>(smem_raw + 288);                // [4 stages][4 builder warps]
-  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + L.red);            // [2][kI8MaxTerms][kI8EpiWarps]
+  unsigned* hkeys = reinterpret_cast<unsigned*>(smem_raw + 384);      // [2 terms][kI8EpiWarps] warp maxima of the peak keys
+  PeakI* red = reinterpret_cast<PeakI*>(smem_raw + L.red);            // [2][J+1][kI8EpiWarps]
+  int2* cand = reinterpret_cast<int2*>(smem_raw + L.cand);            // [2][J+1][16]
+  int* cmeta = reinterpret_cast<int*>(smem_raw + L.cmeta);            // [2][J+1][2]
+  int2* wscr = reinterpret_cast<int2*>(smem_raw + L.wscr);            // [kI8EpiWarps][16]
   unsigned char* stg = smem_raw + L.stg;                              // [kI8EpiWarps][2][kI8StgBytes]
   int* band = reinterpret_cast<int*>(smem_raw + L.band);
   unsigned char* stream = smem_raw + L.stream;
@@ -256,14 +273,21 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], nmma); }
     for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], nmma); }
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * kI8EpiWarps); }
+    mbar_init(hkey, kI8EpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  for (int i = threadIdx.x; i < 4 * nterms; i += blockDim.x) cmeta[i] = 0;
   if (warp == 1) tmem_alloc(tslot, kI8TmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
+  // register budget by role (one setmaxnreg per warpgroup, inside the role's branch so that the
+  // allocation of that branch follows it): the epilogue keeps both tiles' running sums, the
+  // accumulator groups and its addresses in registers; loader / MMA / builder warps need few
+  if (warp < kI8FirstBuild) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(kI8RegsCtl));
   if (warp == 0) {
     // ---------------- loader: band segments (both components) and the term's B images
     if (lane == 0) {
@@ -332,7 +356,9 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         }
         __syncwarp();
       }
+  }
   } else if (warp < kI8FirstEpi) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(kI8RegsBuild));
     // ---------------- builders: int32 band segment -> byte-digit planes (natural order)
     const int tb = threadIdx.x - 32 * kI8FirstBuild;
     uint32_t u = 0;
@@ -395,27 +421,134 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         mbar_arrive(&sfull[ss]);
         mbar_arrive(&bandempty[bs]);
       }
-  } else if (warp < kI8FirstEpi + kI8EpiWarps) {
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(kI8RegsEpi));
     // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
     // kI8HW warps per TMEM lane quarter; warp h of a quarter takes shifts p = PL h .. PL h + PL-1
     // of every lag block, i.e. accumulator columns oc (16 TN) + h (PL TN) + a PL + pl.
-    constexpr int PL = kI8PL, NC = kI8PL * TN;
+    //
+    // Peak search (a7) in two stages.  Stage 1, every lag: the high word of the exact 64-bit
+    // |corr|^2 is a monotone key (m1 >= m2 => hi(m1) >= hi(m2)), so the row's maximum lies among
+    // the lags whose key equals the largest key; each thread keeps the largest key of its lags of
+    // the term (a max tree, no index tracking), the warp maximum is posted to shared memory and
+    // the warp maximum is posted to shared memory and hkey (an mbarrier, one arrival per epilogue
+    // warp and term) is signalled.  Stage 2, once the term's eight warp keys are posted: the first
+    // thread of the first warp holding the largest key copies its 16 running
+    // sums (corr_ti at its lags of both tiles) to the term's candidate slot -- they still hold
+    // corr_ti because stage 2 runs before the next term's D is added (after its accumulator loads,
+    // which hides the wait) -- and the exact comparison (64-bit |.|^2, smallest lag among ties)
+    // over those 16 lags is done once per row in the final combine.  Further threads with the
+    // same key (rare: equal high words) take the exact in-warp search over their warp's lags and
+    // post a warp candidate; every other warp posts an empty one.
+    constexpr int PL = kI8PL;
     const int te = threadIdx.x - 32 * kI8FirstEpi;
-    const int quarter = warp & 3, h = (warp - kI8FirstEpi) >> 2;
+    const int we = warp - kI8FirstEpi;
+    const int quarter = warp & 3, h = we >> 2;
     const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
     const int N = p.N, ntiles = p.ntiles;
     const bool want_corr = p.want_corr != 0, tma = p.tma_store != 0;
-    unsigned char* sbase = stg + (size_t)(warp - kI8FirstEpi) * 2 * kI8StgBytes;
-    uint32_t q = 0, nst = 0;
+    unsigned char* sbase = stg + (size_t)we * 2 * kI8StgBytes;
+    const int tauA = 16 * c + PL * h;                                   // this thread's first lag of tile 0
+    // staging addresses, computed once and kept in registers (opaque to rematerialisation)
+    constexpr int CH = kI8RowBytes / 16;                                // 16-byte chunks per row
+    uint32_t sb_base = smem_u32(sbase), stg_row = sb_base + kI8RowBytes * lane, stg_off[CH];
+    {
+      const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) { stg_off[k] = 16 * (k ^ sw); asm volatile("" : "+r"(stg_off[k])); }
+      asm volatile("" : "+r"(sb_base));
+      asm volatile("" : "+r"(stg_row));
+    }
+    uint32_t q = 0, nst = 0, hn = 0;
     int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      unsigned sr0[PL], si0[PL], sr1[PL], si1[PL];                      // running corr (mod 2^32) of tiles 0, 1
+      // running corr (mod 2^32) of tiles 0, 1, interleaved (re, im) per lag: the staging stores
+      // take four consecutive registers
+      unsigned run0[2 * PL], run1[2 * PL];
+#pragma unroll
+      for (int i = 0; i < 2 * PL; ++i) run1[i] = 0u;                   // one-tile rows: tile 1's lags are all >= N
+      unsigned wh_prev = 0, hm_prev = 0;                                // warp / thread key of the previous term
+      PeakI* rrow = red + (size_t)par * nterms * kI8EpiWarps;
+      const int rowblk = (int)row * nterms * (N >> 4);                  // first lag block of the row's corr
+      // stage 2 for term tip (the term posted last: phase hn - 1 of hkey)
+      auto dump16 = [&](int2* dst) {                                    // this thread's corr_ti at its 16 lags
+        int4* cs = reinterpret_cast<int4*>(dst);
+#pragma unroll
+        for (int k = 0; k < PL / 2; ++k) {
+          cs[k] = make_int4((int)run0[4 * k], (int)run0[4 * k + 1], (int)run0[4 * k + 2], (int)run0[4 * k + 3]);
+          cs[PL / 2 + k] = make_int4((int)run1[4 * k], (int)run1[4 * k + 1], (int)run1[4 * k + 2], (int)run1[4 * k + 3]);
+        }
+      };
+      auto resolve = [&](int tip) {
+        mbar_wait(hkey, (hn - 1) & 1);
+        // the term's largest key; the first warp holding it fills the candidate slot
+        const uint4* hp = reinterpret_cast<const uint4*>(hkeys + kI8EpiWarps * ((hn - 1) & 1));
+        const uint4 ka = hp[0], kb = hp[1];
+        const unsigned kk[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+        const unsigned gmax = max(max(max(ka.x, ka.y), max(ka.z, ka.w)), max(max(kb.x, kb.y), max(kb.z, kb.w)));
+        PeakI* rp = rrow + (size_t)tip * kI8EpiWarps + we;
+        bool posted = false;
+        if (wh_prev == gmax) {
+          unsigned bal = __ballot_sync(0xffffffffu, hm_prev == gmax);   // non-zero: the warp key is some lane's key
+          bool lower = false;                                           // a lower-numbered warp holds the same key
+#pragma unroll
+          for (int w = 0; w < kI8EpiWarps - 1; ++w) lower = lower || (w < we && kk[w] == gmax);
+          if (!lower) {
+            // the term's key holder: first such lane of the first such warp fills the candidate slot
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            if (lane == src) {
+              const int slot = par * nterms + tip;
+              dump16(cand + (size_t)slot * 16);
+              cmeta[2 * slot + 1] = tauA;
+              cmeta[2 * slot] = 1;
+            }
+          }
+          if (bal) {
+            // rare (equal high words): the other holders' lags, exact, 16 lanes per holder
+            PeakI wb;
+            wb.m2 = 0; wb.tau = -1; wb.re = 0; wb.im = 0; wb.pad = 0;
+            int2* ws = wscr + we * 16;
+            while (bal) {
+              const int src = __ffs(bal) - 1;
+              bal &= bal - 1;
+              if (lane == src) dump16(ws);
+              __syncwarp();
+              const int tsrc = 16 * (32 * quarter + src) + PL * h;
+              const int tau = lane < PL ? tsrc + lane : 2048 + tsrc + (lane - PL);
+              const bool ok = lane < 2 * PL && tau < N;
+              const int2 v = ok ? ws[lane] : make_int2(0, 0);
+              const unsigned long long m = mag2i(v.x, v.y);
+              const unsigned hi = ok ? (unsigned)(m >> 32) : 0u, lo = ok ? (unsigned)m : 0u;
+              const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+              const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
+              const unsigned cnd = (ok && hi == mhi && lo == mlo) ? (unsigned)tau : 0xffffffffu;
+              const unsigned tmin = __reduce_min_sync(0xffffffffu, cnd);
+              if (tmin != 0xffffffffu) {
+                const unsigned long long mm = ((unsigned long long)mhi << 32) | mlo;
+                if (wb.tau < 0 || beats(mm, (int)tmin, wb.m2, wb.tau)) {
+                  const int wl = __ffs(__ballot_sync(0xffffffffu, cnd == tmin)) - 1;
+                  wb.m2 = mm; wb.tau = (int)tmin;
+                  wb.re = __shfl_sync(0xffffffffu, v.x, wl);
+                  wb.im = __shfl_sync(0xffffffffu, v.y, wl);
+                }
+              }
+              __syncwarp();
+            }
+            if (lane == 0) *rp = wb;
+            posted = true;
+          }
+        }
+        if (!posted && lane == 0) {
+          PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0;
+          *rp = e;
+        }
+      };
       for (int step = 0; step < nterms; ++step) {
         const int ti = p.J - step;
-        PeakI best;
-        best.m2 = 0; best.tau = -1; best.re = 0; best.im = 0; best.pad = 0;
-        // one tile: D_ti (digits recombined mod 2^32) added into the running sums (sr, si)
-        auto tile = [&](int t, unsigned (&sr)[PL], unsigned (&si)[PL]) {
+        unsigned hmax = 0;                                              // stage 1: largest key of this thread's lags
+        // one tile: D_ti (digits recombined mod 2^32) added into the running sums
+        auto tile = [&](int t, unsigned (&run)[2 * PL]) {
           const uint32_t buf = q % NBUF;
           mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
@@ -450,79 +583,104 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
           ++q;
-          const int tau0 = 2048 * t + 16 * c + PL * h;
+          // the previous term's stage 2 reads the running sums before this term is added
+          if (t == 0 && step > 0) resolve(ti + 1);
+          const int tau0 = 2048 * t + tauA;
 #pragma unroll
           for (int i = 0; i < PL; ++i) {
-            if (step == 0) { sr[i] = re[i]; si[i] = im[i]; }
-            else { sr[i] += re[i]; si[i] += im[i]; }
+            if (step == 0) { run[2 * i] = re[i]; run[2 * i + 1] = im[i]; }
+            else { run[2 * i] += re[i]; run[2 * i + 1] += im[i]; }
           }
           if (want_corr && !tma && tau0 < N) {
             int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tau0);
 #pragma unroll
             for (int i = 0; i < PL / 2; ++i)
-              dst[i] = make_int4((int)sr[2 * i], (int)si[2 * i], (int)sr[2 * i + 1], (int)si[2 * i + 1]);
+              dst[i] = make_int4((int)run[4 * i], (int)run[4 * i + 1], (int)run[4 * i + 2], (int)run[4 * i + 3]);
           }
           if (want_corr && tma) {
             // corr_ti of this warp's 32 lag blocks (PL lags each) -> swizzled staging (the TMA map's
             // swizzle span = one lane's row) -> one TMA tensor store; the staging buffer of two
             // stores ago must have been read
-            unsigned char* sb = sbase + (nst & 1) * kI8StgBytes;
+            const uint32_t sb = stg_row + (nst & 1) * kI8StgBytes;      // this lane's row of the staging buffer
             if (lane == 0) bulk_wait_read_le1();
             __syncwarp();
-            constexpr int CH = kI8RowBytes / 16;                        // 16-byte chunks per row
-            const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
 #pragma unroll
             for (int k = 0; k < CH; ++k)
-              *reinterpret_cast<int4*>(sb + kI8RowBytes * lane + 16 * (k ^ sw)) =
-                  make_int4((int)sr[2 * k], (int)si[2 * k], (int)sr[2 * k + 1], (int)si[2 * k + 1]);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n"
+                           :: "r"(sb + stg_off[k]), "r"(run[4 * k]), "r"(run[4 * k + 1]), "r"(run[4 * k + 2]), "r"(run[4 * k + 3])
+                           : "memory");
+          }
+          if (tau0 < N) {
+            // stage 1: keys of this tile's lags (max tree); independent work under the staging stores
+            unsigned k8[PL];
+#pragma unroll
+            for (int i = 0; i < PL; ++i) k8[i] = (unsigned)(mag2i((int)run[2 * i], (int)run[2 * i + 1]) >> 32);
+#pragma unroll
+            for (int w = PL / 2; w >= 1; w >>= 1)
+#pragma unroll
+              for (int i = 0; i < w; ++i) k8[i] = max(k8[i], k8[i + w]);
+            hmax = max(hmax, k8[0]);
+          }
+          if (want_corr && tma) {
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's 32 blocks all in or all out
-              const long long blk = (((long long)row * nterms + ti) * N + 2048 * t + 512 * quarter) >> 4;
-              tma_store_3d(&p.cmap, smem_u32(sb), 0, h, (int)blk);
+              // lag-block coordinate of (row, ti, tile t, quarter); the tensor's block count fits 32 bits
+              const int blk = (rowblk + ti * (N >> 4)) + 128 * t + 32 * quarter;
+              tma_store_3d(&p.cmap, sb_base + (nst & 1) * kI8StgBytes, 0, h, blk);
               bulk_commit();
             }
             ++nst;
           }
-          if (tau0 < N) {
-            // peak candidates in lag order: strict '>' keeps the smallest lag of a tie
-            if (best.tau < 0) { best.m2 = mag2i((int)sr[0], (int)si[0]); best.tau = tau0; best.re = (int)sr[0]; best.im = (int)si[0]; }
-#pragma unroll
-            for (int i = 0; i < PL; ++i) {
-              const unsigned long long m = mag2i((int)sr[i], (int)si[i]);
-              const bool gt = m > best.m2;
-              best.m2 = gt ? m : best.m2;
-              best.tau = gt ? tau0 + i : best.tau;
-              best.re = gt ? (int)sr[i] : best.re;
-              best.im = gt ? (int)si[i] : best.im;
-            }
-          }
         };
-        tile(0, sr0, si0);
-        if (ntiles > 1) tile(1, sr1, si1);
-        // the row's peak at scale ti: warp argmax (high word, low word, smallest lag) -> partial
-        const bool ok = best.tau >= 0;
-        const unsigned hi = ok ? (unsigned)(best.m2 >> 32) : 0u, lo = ok ? (unsigned)best.m2 : 0u;
-        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-        const unsigned mlo = __reduce_max_sync(0xffffffffu, (ok && hi == mhi) ? lo : 0u);
-        const unsigned cand = (ok && hi == mhi && lo == mlo) ? (unsigned)best.tau : 0xffffffffu;
-        const unsigned tmin = __reduce_min_sync(0xffffffffu, cand);
-        PeakI* rp = red + ((size_t)par * kI8MaxTerms + ti) * kI8EpiWarps;
-        if (ok && (unsigned)best.tau == tmin) rp[warp - kI8FirstEpi] = best;
-        else if (lane == 0 && tmin == 0xffffffffu) { PeakI e; e.m2 = 0; e.tau = -1; e.re = 0; e.im = 0; e.pad = 0; rp[warp - kI8FirstEpi] = e; }
-      }
-      // every scale of the row: combine the warps' partials (one barrier per row)
-      named_bar(2, 32 * kI8EpiWarps);
-      if (te < nterms && lag) {
-        const PeakI* rp = red + ((size_t)par * kI8MaxTerms + te) * kI8EpiWarps;
-        PeakI b = rp[0];
-        for (int w = 1; w < kI8EpiWarps; ++w) {
-          const PeakI o = rp[w];
-          if (o.tau >= 0 && (b.tau < 0 || beats(o.m2, o.tau, b.m2, b.tau))) b = o;
+        tile(0, run0);
+        if (ntiles > 1) tile(1, run1);
+        // post this warp's key for the term
+        const unsigned wh = __reduce_max_sync(0xffffffffu, hmax);
+        if (lane == 0) {
+          hkeys[kI8EpiWarps * (hn & 1) + we] = wh;
+          mbar_arrive(hkey);
         }
-        const size_t e = (size_t)row * nterms + te;
-        lag[e] = b.tau;
-        if (val) val[e] = make_int2(b.re, b.im);
+        ++hn;
+        wh_prev = wh;
+        hm_prev = hmax;
+        if (step == nterms - 1) resolve(ti);                            // the row's last term: no later tile hides the wait
+      }
+      // every scale of the row: combine the warps' candidates (one barrier per row)
+      named_bar(2, 32 * kI8EpiWarps);
+      // 16 lanes per term: lane j takes the key holder's lag j (exact |.|^2) and, for j < 8, warp j's
+      // tie candidate; half-warp argmax (largest |.|^2, smallest lag among ties)
+      for (int tt = te >> 4; tt < nterms; tt += 2 * kI8EpiWarps) {
+        const int j = lane & 15;
+        const unsigned hmask = 0xffffu << (lane & 16);
+        unsigned long long m = 0;
+        int tau = -1, vre = 0, vim = 0;
+        int* cm = cmeta + 2 * (par * nterms + tt);
+        if (cm[0]) {
+          const int tA = cm[1];
+          const int tj = j < PL ? tA + j : 2048 + tA + (j - PL);
+          if (tj < N) {
+            const int2 v = cand[(size_t)(par * nterms + tt) * 16 + j];
+            m = mag2i(v.x, v.y); tau = tj; vre = v.x; vim = v.y;
+          }
+        }
+        if (j < kI8EpiWarps) {
+          const PeakI o = rrow[(size_t)tt * kI8EpiWarps + j];
+          if (o.tau >= 0 && (tau < 0 || beats(o.m2, o.tau, m, tau))) { m = o.m2; tau = o.tau; vre = o.re; vim = o.im; }
+        }
+        const bool ok = tau >= 0;
+        const unsigned hi = ok ? (unsigned)(m >> 32) : 0u, lo = ok ? (unsigned)m : 0u;
+        const unsigned mhi = __reduce_max_sync(hmask, hi);
+        const unsigned mlo = __reduce_max_sync(hmask, (ok && hi == mhi) ? lo : 0u);
+        const unsigned cnd = (ok && hi == mhi && lo == mlo) ? (unsigned)tau : 0xffffffffu;
+        const unsigned tmin = __reduce_min_sync(hmask, cnd);
+        __syncwarp(hmask);
+        if (j == 0) cm[0] = 0;
+        if (lag && ((ok && (unsigned)tau == tmin) || (j == 0 && tmin == 0xffffffffu))) {
+          const size_t e = (size_t)row * nterms + tt;
+          lag[e] = tmin == 0xffffffffu ? -1 : tau;
+          if (val) val[e] = tmin == 0xffffffffu ? make_int2(0, 0) : make_int2(vre, vim);
+        }
       }
       par ^= 1;
     }
