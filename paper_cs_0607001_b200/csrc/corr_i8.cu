@@ -54,12 +54,15 @@
 
 namespace sidwt {
 
-// epilogue: kI8HW warps per TMEM lane quarter, each kI8PL of the 16 shifts of every lag block
-constexpr int kI8HW = 2, kI8PL = 16 / kI8HW;     // measured: 4 warps per quarter issue-bound (C5 corr 9.05 vs 8.38 ms)
-static_assert(kI8HW == 2, "accumulator column order n = 32 a + 16 (p / 8) + 8 oc + p % 8 assumes two halves");
+// epilogue: one warp per TMEM lane quarter and tile; a thread owns a whole lag block (16 lags) of
+// its tile, so the per-tile fixed work (waits, fence, TMA issue) is paid once per 16 lags; the two
+// tiles of a row are taken by two groups of four warps in parallel (measured before the epilogue
+// had its own register budget: two warps per quarter with 8 lags each, both tiles in sequence)
+constexpr int kI8HW = 1, kI8PL = 16 / kI8HW;
+constexpr int kI8TileGroups = 2;                   // tiles of a row handled in parallel (ntiles <= 2)
 // roles by warpgroup (setmaxnreg moves registers between warpgroups): warps 0-3 loader, two MMA
 // issuers and one idle warp; warps 4-7 builders; warps 8-15 epilogue
-constexpr int kI8FirstBuild = 4, kI8BuildWarps = 4, kI8FirstEpi = 8, kI8EpiWarps = 4 * kI8HW;
+constexpr int kI8FirstBuild = 4, kI8BuildWarps = 4, kI8FirstEpi = 8, kI8EpiWarps = 4 * kI8TileGroups;
 constexpr int kI8Mma2 = 2;                               // second MMA-issuing warp
 constexpr int kI8Warps = kI8FirstEpi + kI8EpiWarps;
 constexpr int kI8RegsCtl = 56, kI8RegsBuild = 72, kI8RegsEpi = 192;   // per thread, after setmaxnreg
@@ -83,7 +86,7 @@ __host__ __device__ inline I8Smem i8_layout(const I8Params& p) {
   L.cmeta = L.cand + 2 * nterms * 16 * 8;                               // [2 rows][J+1] (taken, first lag)
   L.wscr = (L.cmeta + 2 * nterms * 8 + 15) & ~(size_t)15;               // [kI8EpiWarps][16 lags] int2: scratch of the rare tie path
   L.stg = (L.wscr + (size_t)kI8EpiWarps * 16 * 8 + 1023) & ~(size_t)1023;   // swizzled TMA staging
-  L.band = L.stg + (size_t)kI8EpiWarps * 2 * kI8StgBytes;
+  L.band = L.stg + (size_t)kI8EpiWarps * kI8StgBytes;
   L.stream = (L.band + (size_t)p.nband * 2 * p.seg_alloc * 4 + 127) & ~(size_t)127;
   L.img = L.stream + (size_t)p.nstream * 2 * p.dmax * p.plane;
   L.total = L.img + (size_t)p.nimg * p.img_alloc;
@@ -255,7 +258,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   int2* cand = reinterpret_cast<int2*>(smem_raw + L.cand);            // [2][J+1][16]
   int* cmeta = reinterpret_cast<int*>(smem_raw + L.cmeta);            // [2][J+1][2]
   int2* wscr = reinterpret_cast<int2*>(smem_raw + L.wscr);            // [kI8EpiWarps][16]
-  unsigned char* stg = smem_raw + L.stg;                              // [kI8EpiWarps][2][kI8StgBytes]
+  unsigned char* stg = smem_raw + L.stg;                              // [kI8EpiWarps][kI8StgBytes]
   int* band = reinterpret_cast<int*>(smem_raw + L.band);
   unsigned char* stream = smem_raw + L.stream;
   unsigned char* imgs = smem_raw + L.img;
@@ -272,7 +275,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
     for (int i = 0; i < NB; ++i) { mbar_init(&bandfull[i], 1); mbar_init(&bandempty[i], kI8BuildThreads); }
     for (int i = 0; i < NS; ++i) { mbar_init(&sfull[i], kI8BuildThreads); mbar_init(&sempty[i], nmma); }
     for (int i = 0; i < NI; ++i) { mbar_init(&imgfull[i], 1); mbar_init(&imgempty[i], nmma); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * kI8EpiWarps); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 32 * 4); }
     mbar_init(hkey, kI8EpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -424,34 +427,34 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(kI8RegsEpi));
     // ---------------- epilogue: TMEM -> digits recombined -> eq. (4) running sums -> corr, peaks.
-    // kI8HW warps per TMEM lane quarter; warp h of a quarter takes shifts p = PL h .. PL h + PL-1
-    // of every lag block, i.e. accumulator columns oc (16 TN) + h (PL TN) + a PL + pl.
+    // Warp (quarter, tg): TMEM lanes 32 quarter .. +31 of tile tg; lane = one lag block, all 16
+    // shifts: accumulator columns 32 c + 16 half + 8 oc + i of digit-weight group c.
     //
     // Peak search (a7) in two stages.  Stage 1, every lag: the high word of the exact 64-bit
     // |corr|^2 is a monotone key (m1 >= m2 => hi(m1) >= hi(m2)), so the row's maximum lies among
-    // the lags whose key equals the largest key; each thread keeps the largest key of its lags of
-    // the term (a max tree, no index tracking), the warp maximum is posted to shared memory and
-    // the warp maximum is posted to shared memory and hkey (an mbarrier, one arrival per epilogue
-    // warp and term) is signalled.  Stage 2, once the term's eight warp keys are posted: the first
-    // thread of the first warp holding the largest key copies its 16 running
-    // sums (corr_ti at its lags of both tiles) to the term's candidate slot -- they still hold
+    // the lags whose key equals the largest key; each thread keeps the largest key of its 16 lags
+    // (a max tree, no index tracking), the warp maximum is posted to shared memory and hkey (an
+    // mbarrier, one arrival per epilogue warp and term) is signalled.  Stage 2, once the term's
+    // eight warp keys are posted: the first thread of the first warp holding the largest key copies
+    // its 16 running sums (corr_ti at its lags) to the term's candidate slot -- they still hold
     // corr_ti because stage 2 runs before the next term's D is added (after its accumulator loads,
     // which hides the wait) -- and the exact comparison (64-bit |.|^2, smallest lag among ties)
     // over those 16 lags is done once per row in the final combine.  Further threads with the
-    // same key (rare: equal high words) take the exact in-warp search over their warp's lags and
-    // post a warp candidate; every other warp posts an empty one.
+    // same key (rare: equal high words) are compared exactly in their warp (16 lanes per holder)
+    // and post a warp candidate; every other warp posts an empty one.
     constexpr int PL = kI8PL;
     const int te = threadIdx.x - 32 * kI8FirstEpi;
     const int we = warp - kI8FirstEpi;
-    const int quarter = warp & 3, h = we >> 2;
+    const int quarter = warp & 3, tg = we >> 2;
     const int c = 32 * quarter + lane;                                  // TMEM lane = lag block of the tile
     const int N = p.N, ntiles = p.ntiles;
     const bool want_corr = p.want_corr != 0, tma = p.tma_store != 0;
-    unsigned char* sbase = stg + (size_t)we * 2 * kI8StgBytes;
-    const int tauA = 16 * c + PL * h;                                   // this thread's first lag of tile 0
+    const bool mine = tg < ntiles;                                      // this warp's tile exists
+    const int tauA = 2048 * tg + 16 * c;                                // this thread's first lag
+    const bool valid = mine && tauA < N;                                // N % 16 == 0: a block is all in or all out
     // staging addresses, computed once and kept in registers (opaque to rematerialisation)
     constexpr int CH = kI8RowBytes / 16;                                // 16-byte chunks per row
-    uint32_t sb_base = smem_u32(sbase), stg_row = sb_base + kI8RowBytes * lane, stg_off[CH];
+    uint32_t sb_base = smem_u32(stg + (size_t)we * kI8StgBytes), stg_row = sb_base + kI8RowBytes * lane, stg_off[CH];
     {
       const int sw = ((lane * kI8RowBytes) >> 7) & (CH - 1);
 #pragma unroll
@@ -459,26 +462,24 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       asm volatile("" : "+r"(sb_base));
       asm volatile("" : "+r"(stg_row));
     }
-    uint32_t q = 0, nst = 0, hn = 0;
+    uint32_t q = (uint32_t)tg, hn = 0;                                  // q: this warp's tile in the MMA order
     int par = 0;
     for (long long row = blockIdx.x; row < p.rows; row += gridDim.x) {
-      // running corr (mod 2^32) of tiles 0, 1, interleaved (re, im) per lag: the staging stores
+      // running corr (mod 2^32) of the thread's 16 lags, interleaved (re, im): the staging stores
       // take four consecutive registers
-      unsigned run0[2 * PL], run1[2 * PL];
+      unsigned run[2 * PL];
 #pragma unroll
-      for (int i = 0; i < 2 * PL; ++i) run1[i] = 0u;                   // one-tile rows: tile 1's lags are all >= N
+      for (int i = 0; i < 2 * PL; ++i) run[i] = 0u;
       unsigned wh_prev = 0, hm_prev = 0;                                // warp / thread key of the previous term
       PeakI* rrow = red + (size_t)par * nterms * kI8EpiWarps;
       const int rowblk = (int)row * nterms * (N >> 4);                  // first lag block of the row's corr
-      // stage 2 for term tip (the term posted last: phase hn - 1 of hkey)
       auto dump16 = [&](int2* dst) {                                    // this thread's corr_ti at its 16 lags
         int4* cs = reinterpret_cast<int4*>(dst);
 #pragma unroll
-        for (int k = 0; k < PL / 2; ++k) {
-          cs[k] = make_int4((int)run0[4 * k], (int)run0[4 * k + 1], (int)run0[4 * k + 2], (int)run0[4 * k + 3]);
-          cs[PL / 2 + k] = make_int4((int)run1[4 * k], (int)run1[4 * k + 1], (int)run1[4 * k + 2], (int)run1[4 * k + 3]);
-        }
+        for (int k = 0; k < PL / 2; ++k)
+          cs[k] = make_int4((int)run[4 * k], (int)run[4 * k + 1], (int)run[4 * k + 2], (int)run[4 * k + 3]);
       };
+      // stage 2 for term tip (the term posted last: phase hn - 1 of hkey)
       auto resolve = [&](int tip) {
         mbar_wait(hkey, (hn - 1) & 1);
         // the term's largest key; the first warp holding it fills the candidate slot
@@ -514,9 +515,8 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
               bal &= bal - 1;
               if (lane == src) dump16(ws);
               __syncwarp();
-              const int tsrc = 16 * (32 * quarter + src) + PL * h;
-              const int tau = lane < PL ? tsrc + lane : 2048 + tsrc + (lane - PL);
-              const bool ok = lane < 2 * PL && tau < N;
+              const int tau = 2048 * tg + 16 * (32 * quarter + src) + lane;
+              const bool ok = lane < PL && tau < N && mine;
               const int2 v = ok ? ws[lane] : make_int2(0, 0);
               const unsigned long long m = mag2i(v.x, v.y);
               const unsigned hi = ok ? (unsigned)(m >> 32) : 0u, lo = ok ? (unsigned)m : 0u;
@@ -547,94 +547,97 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
       for (int step = 0; step < nterms; ++step) {
         const int ti = p.J - step;
         unsigned hmax = 0;                                              // stage 1: largest key of this thread's lags
-        // one tile: D_ti (digits recombined mod 2^32) added into the running sums
-        auto tile = [&](int t, unsigned (&run)[2 * PL]) {
+        unsigned re[PL], im[PL];
+        if (mine) {
+          // this warp's tile: D_ti (digits recombined mod 2^32)
           const uint32_t buf = q % NBUF;
+          // a single TMEM buffer alternates between the two tile groups: pass the other group's phase first
+          if (NBUF == 1 && ntiles > 1 && q > 0) mbar_wait(&dfull[0], (q - 1) & 1);
           mbar_wait(&dfull[buf], (q / NBUF) & 1);
           tc_fence_after();
           const int D = dcnt[buf];
-          // group c at columns 32 c + 16 h + [oc 8 + pl]: one x16 load per group
-          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols + 16 * h;
-          unsigned re[PL], im[PL];
-          {
+          const uint32_t tb0 = tmem + ((uint32_t)(32 * quarter) << 16) + buf * bufcols;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            // digit-weight group c, half hf at columns 32 c + 16 hf + [oc 8 + i]: one x16 load per group;
             // groups 0, 1 always exist (D >= 2), group 2 whenever TN >= 2
             uint32_t g0[16], g1[16], g2[16];
-            tmem_ld_cols<16>(tb0, g0);
-            tmem_ld_cols<16>(tb0 + 32, g1);
-            if constexpr (TN >= 2) tmem_ld_cols<16>(tb0 + 64, g2);
+            tmem_ld_cols<16>(tb0 + 16 * hf, g0);
+            tmem_ld_cols<16>(tb0 + 16 * hf + 32, g1);
+            if constexpr (TN >= 2) tmem_ld_cols<16>(tb0 + 16 * hf + 64, g2);
             tmem_wait_ld_all();
             tie_regs(g0); tie_regs(g1);
             if constexpr (TN >= 2) tie_regs(g2);
 #pragma unroll
-            for (int i = 0; i < PL; ++i) {
-              re[i] = g0[i] + (g1[i] << 8);
-              im[i] = g0[8 + i] + (g1[8 + i] << 8);
-              if constexpr (TN >= 2) { re[i] += g2[i] << 16; im[i] += g2[8 + i] << 16; }
+            for (int i = 0; i < 8; ++i) {
+              re[8 * hf + i] = g0[i] + (g1[i] << 8);
+              im[8 * hf + i] = g0[8 + i] + (g1[8 + i] << 8);
+              if constexpr (TN >= 2) { re[8 * hf + i] += g2[i] << 16; im[8 * hf + i] += g2[8 + i] << 16; }
             }
           }
           for (int cq = TN >= 2 ? 3 : 2; cq < D + TN - 1; ++cq) {      // rare: higher digit-weight groups
-            uint32_t g[16];
-            tmem_ld_cols<16>(tb0 + 32 * cq, g);
-            tmem_wait_ld_all();
-            tie_regs(g);
 #pragma unroll
-            for (int i = 0; i < PL; ++i) { re[i] += g[i] << (8 * cq); im[i] += g[8 + i] << (8 * cq); }
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t g[16];
+              tmem_ld_cols<16>(tb0 + 16 * hf + 32 * cq, g);
+              tmem_wait_ld_all();
+              tie_regs(g);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) { re[8 * hf + i] += g[i] << (8 * cq); im[8 * hf + i] += g[8 + i] << (8 * cq); }
+            }
           }
           tc_fence_before();
           mbar_arrive(&dempty[buf]);
-          ++q;
-          // the previous term's stage 2 reads the running sums before this term is added
-          if (t == 0 && step > 0) resolve(ti + 1);
-          const int tau0 = 2048 * t + tauA;
+          q += (uint32_t)ntiles;
+        }
+        // the previous term's stage 2 reads the running sums before this term is added
+        if (step > 0) resolve(ti + 1);
+        if (mine) {
 #pragma unroll
           for (int i = 0; i < PL; ++i) {
             if (step == 0) { run[2 * i] = re[i]; run[2 * i + 1] = im[i]; }
             else { run[2 * i] += re[i]; run[2 * i + 1] += im[i]; }
           }
-          if (want_corr && !tma && tau0 < N) {
-            int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tau0);
+          if (want_corr && !tma && valid) {
+            int4* dst = reinterpret_cast<int4*>(corr + ((size_t)row * nterms + ti) * N + tauA);
 #pragma unroll
             for (int i = 0; i < PL / 2; ++i)
               dst[i] = make_int4((int)run[4 * i], (int)run[4 * i + 1], (int)run[4 * i + 2], (int)run[4 * i + 3]);
           }
           if (want_corr && tma) {
-            // corr_ti of this warp's 32 lag blocks (PL lags each) -> swizzled staging (the TMA map's
-            // swizzle span = one lane's row) -> one TMA tensor store; the staging buffer of two
-            // stores ago must have been read
-            const uint32_t sb = stg_row + (nst & 1) * kI8StgBytes;      // this lane's row of the staging buffer
-            if (lane == 0) bulk_wait_read_le1();
+            // corr_ti of this warp's 32 lag blocks (4 KB contiguous in HBM) -> swizzled staging (the
+            // TMA map's swizzle span = one lane's row) -> one TMA tensor store; the previous term's
+            // store must have read the staging buffer
+            if (lane == 0) bulk_wait_read_all();
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < CH; ++k)
               asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n"
-                           :: "r"(sb + stg_off[k]), "r"(run[4 * k]), "r"(run[4 * k + 1]), "r"(run[4 * k + 2]), "r"(run[4 * k + 3])
+                           :: "r"(stg_row + stg_off[k]), "r"(run[4 * k]), "r"(run[4 * k + 1]), "r"(run[4 * k + 2]), "r"(run[4 * k + 3])
                            : "memory");
           }
-          if (tau0 < N) {
+          if (valid) {
             // stage 1: keys of this tile's lags (max tree); independent work under the staging stores
-            unsigned k8[PL];
+            unsigned k16[PL];
 #pragma unroll
-            for (int i = 0; i < PL; ++i) k8[i] = (unsigned)(mag2i((int)run[2 * i], (int)run[2 * i + 1]) >> 32);
+            for (int i = 0; i < PL; ++i) k16[i] = (unsigned)(mag2i((int)run[2 * i], (int)run[2 * i + 1]) >> 32);
 #pragma unroll
             for (int w = PL / 2; w >= 1; w >>= 1)
 #pragma unroll
-              for (int i = 0; i < w; ++i) k8[i] = max(k8[i], k8[i + w]);
-            hmax = max(hmax, k8[0]);
+              for (int i = 0; i < w; ++i) k16[i] = max(k16[i], k16[i + w]);
+            hmax = k16[0];
           }
           if (want_corr && tma) {
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0 && 2048 * t + 512 * quarter < N) {   // N % 512 == 0: a warp's 32 blocks all in or all out
-              // lag-block coordinate of (row, ti, tile t, quarter); the tensor's block count fits 32 bits
-              const int blk = (rowblk + ti * (N >> 4)) + 128 * t + 32 * quarter;
-              tma_store_3d(&p.cmap, sb_base + (nst & 1) * kI8StgBytes, 0, h, blk);
+            if (lane == 0 && 2048 * tg + 512 * quarter < N) {   // N % 512 == 0: a warp's 32 blocks all in or all out
+              // lag-block coordinate of (row, ti, tile, quarter); the tensor's block count fits 32 bits
+              const int blk = (rowblk + ti * (N >> 4)) + 128 * tg + 32 * quarter;
+              tma_store_3d(&p.cmap, sb_base, 0, 0, blk);
               bulk_commit();
             }
-            ++nst;
           }
-        };
-        tile(0, run0);
-        if (ntiles > 1) tile(1, run1);
+        }
         // post this warp's key for the term
         const unsigned wh = __reduce_max_sync(0xffffffffu, hmax);
         if (lane == 0) {
@@ -643,10 +646,10 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         }
         ++hn;
         wh_prev = wh;
-        hm_prev = hmax;
+        hm_prev = valid ? hmax : 0xffffffffu;                           // a thread without lags never holds the key
         if (step == nterms - 1) resolve(ti);                            // the row's last term: no later tile hides the wait
       }
-      // every scale of the row: combine the warps' candidates (one barrier per row)
+      // every scale of the row: combine the candidates (one barrier per row)
       named_bar(2, 32 * kI8EpiWarps);
       // 16 lanes per term: lane j takes the key holder's lag j (exact |.|^2) and, for j < 8, warp j's
       // tie candidate; half-warp argmax (largest |.|^2, smallest lag among ties)
@@ -657,8 +660,7 @@ k_correlate_i8(const int* __restrict__ bands, const unsigned char* __restrict__ 
         int tau = -1, vre = 0, vim = 0;
         int* cm = cmeta + 2 * (par * nterms + tt);
         if (cm[0]) {
-          const int tA = cm[1];
-          const int tj = j < PL ? tA + j : 2048 + tA + (j - PL);
+          const int tj = cm[1] + j;
           if (tj < N) {
             const int2 v = cand[(size_t)(par * nterms + tt) * 16 + j];
             m = mag2i(v.x, v.y); tau = tj; vre = v.x; vim = v.y;
