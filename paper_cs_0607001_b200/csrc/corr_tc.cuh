@@ -212,6 +212,8 @@ constexpr int kTcFirstBuild = 3;         // warp 2: band stager
 constexpr int kTcFirstEpi = kTcFirstBuild + kTcBuildWarps;
 constexpr int kTcWarps = kTcFirstEpi + kTcEpiWarps;
 constexpr int kTcThreads = 32 * kTcWarps;
+constexpr int kTcRegsProd = 96, kTcRegsEpi = 160;   // registers per thread after setmaxnreg (8 warps each: 8 x 96 + 8 x 160 = 2048)
+static_assert(kTcFirstEpi == 8 && kTcWarps == 16, "setmaxnreg: the epilogue is warpgroups 2-3");
 
 struct TcSmem {
   int ring, zbuf, stg, epi, total;
@@ -268,6 +270,13 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" :: "r"(smem_u32(bar)) : "memory");
+}
+// per-warpgroup register budget: the kernels launch with 512 threads x 128 registers; a role's
+// warpgroups release registers (dec) or take the released ones (inc)
+template <int N>
+__device__ __forceinline__ void set_max_regs() {
+  if constexpr (N > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(N));
+  else if constexpr (N < 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(N));
 }
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" :: "r"(id), "r"(n) : "memory");
@@ -361,6 +370,10 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
     ph_ = ph0;
     while (s_ >= S) { s_ -= S; ph_ ^= 1u; }
   };
+  // register budget by role (whole warpgroups 0-1 producers, 2-3 epilogue; setmaxnreg at the head
+  // of each arm so that the arm's allocation follows it)
+  if (warp < kTcFirstEpi) {
+  set_max_regs<kTcRegsProd>();
   if (warp == 0) {
     // ===================== template operand producer =====================
     if (lane == 0) {
@@ -570,7 +583,9 @@ k_correlate_tc(const float* __restrict__ bands, const unsigned char* __restrict_
     if (p.prof && blockIdx.x == 0 && bt == 0)
       printf("[tc prof] builder: total %lld  wait_stg %lld  wait_zempty %lld  convert %lld\n",
              TC_CLOCK() - t_start, w_stg, w_ze, b_conv);
+  }
   } else {
+    set_max_regs<kTcRegsEpi>();
     // ===================== epilogue (8 warps; TMEM lane group = warp & 3) =====================
     // Per 32-lag chunk, two 16x256b TMEM loads (lane blocks k = 0, 1 of the warp's 32 lanes)
     // give thread (a, b) the complex values of templates tr[k] = 8 k + (b >> 1) + 4 (b & 1)

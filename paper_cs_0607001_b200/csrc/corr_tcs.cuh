@@ -52,6 +52,7 @@ namespace sidwt {
 
 constexpr int kTcsWarps = 16;
 constexpr int kTcsThreads = 32 * kTcsWarps;
+constexpr int kTcsRegsProd = 160, kTcsRegsEpi = 96;   // registers per thread after setmaxnreg (8 x prod + 8 x epi = 2048)
 constexpr int kTcsFirstConv = 2, kTcsConvWarps = 6;     // 3 warps (96 threads) per plane
 constexpr int kTcsConvThreads = 96;
 constexpr int kTcsFirstEpi = 8, kTcsEpiWarps = 8, kTcsEpiThreads = 32 * kTcsEpiWarps;
@@ -307,6 +308,10 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
+  // register budget by role (whole warpgroups 0-1 loader / MMA / converters, 2-3 epilogue; setmaxnreg
+  // at the head of each arm so that the arm's allocation follows it)
+  if (warp < kTcsFirstEpi) {
+  set_max_regs<kTcsRegsProd>();
   if (warp == 0) {
     // ---------------- template operand producer
     if (lane == 0) {
@@ -413,7 +418,9 @@ k_correlate_tcs(const float* __restrict__ bands, const unsigned char* __restrict
         else tcs_convert<2>(p, tm, tc, src, buf, &bfull[bs], &bempty[bs], par, w_be);
       }
     if (p.prof && blockIdx.x == 0 && tc == 0) printf("tcs cta0 converter %d: wait bempty %lld\n", pl, w_be);
+  }
   } else {
+    set_max_regs<kTcsRegsEpi>();
     // ---------------- epilogue (256 threads): TMEM lane quarter = warp % 4 (data rows n),
     // half h = shifts p in [32 h, 32 h + 32)
     const int te = threadIdx.x - 32 * kTcsFirstEpi;
