@@ -76,6 +76,32 @@ def test_wide_template_three_digits():
     _check(J, N, rows, tm)
 
 
+@pytest.mark.parametrize("J,N", [(3, 4096), (8, 4096), (4, 2048), (2, 512)])
+def test_peak_search_ties_and_equal_keys(J, N):
+    """The two-stage peak search (32-bit high-word keys, exact 64-bit comparison for the key
+    holders): rows whose |corr|^2 stays below 2^32 (every key 0: every thread is a holder), an
+    all-zero row, a DC row, an impulse, and rows periodic in N/2 and N/8 (exactly equal maxima in
+    different lag blocks, warps and tiles: the smallest lag must win) -- bit-identical to the
+    oracle and to the SIMT kernel."""
+    rng = np.random.default_rng(100 * J + N)
+    T = 40
+    tiny_t = rng.integers(-3, 4, size=(1, T, 2)).astype(np.int16)
+    rows = np.zeros((6, N, 2), dtype=np.int16)
+    rows[0] = rng.integers(-3, 4, size=(N, 2))                       # tiny: all keys 0
+    rows[2, :, 0] = 5                                                # DC (row 1 stays all-zero)
+    rows[3, N // 3] = (7, -2)                                        # impulse
+    rows[4] = np.tile(rng.integers(-3, 4, size=(N // 2, 2)), (2, 1))   # period N/2
+    rows[5] = np.tile(rng.integers(-3, 4, size=(N // 8, 2)), (8, 1))   # period N/8
+    _check(J, N, rows, tiny_t)
+    # the same periodic structure at full scale (keys differ, maxima still exactly equal)
+    big_t = rng.integers(-2047, 2048, size=(1, T, 2)).astype(np.int16)
+    rows2 = np.zeros((3, N, 2), dtype=np.int16)
+    rows2[0] = np.tile(rng.integers(-3000, 3000, size=(N // 2, 2)), (2, 1))
+    rows2[1] = np.tile(rng.integers(-3000, 3000, size=(N // 8, 2)), (8, 1))
+    rows2[2] = np.tile(rng.integers(-3000, 3000, size=(16, 2)), (N // 16, 1))
+    _check(J, N, rows2, big_t)
+
+
 def test_peaks_only_and_many_rows():
     """More rows than SMs (persistent CTAs loop), peaks-only equals the with-corr peaks."""
     import torch
