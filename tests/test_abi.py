@@ -50,6 +50,9 @@ def test_sass_is_sm100a(native):
     # integer family: int8 tcgen05.mma (UTCIMMA), tcgen05.ld, bulk loads, TMA tensor stores of corr
     for k in ("UTCIMMA", "LDTM", "UTMASTG", "UBLKCP"):
         assert per["k_correlate_i8"][k] > 0, ("k_correlate_i8", k)
+    # per-role register budgets (setmaxnreg) in the three warp-specialised tensor-core kernels
+    for kern in ("k_correlate_tc", "k_correlate_tcs", "k_correlate_i8"):
+        assert per[kern]["USETMAXREG"] >= 2, (kern, "USETMAXREG")
     assert per["k_analyze"]["UBLKCP"] > 0                  # TMA bulk stores of the bands
     assert per["k_correlate"]["FFMA2"] > 0                 # packed FP32 real-template correlation
 

@@ -8,7 +8,7 @@ import re
 import subprocess
 import sys
 
-MNEMONICS = ("UTCHMMA", "UTCIMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UTMASTG", "UTMALDG", "UBLKCP", "FFMA2",
+MNEMONICS = ("UTCHMMA", "UTCIMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UTMASTG", "UTMALDG", "UBLKCP", "USETMAXREG", "FFMA2",
              "IMAD", "PRMT", "SYNCS")
 
 
