@@ -50,6 +50,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 namespace sidwt {
@@ -783,7 +785,14 @@ bool i8_configure(I8Params& p, int N, int J, int stride, int ML, const int* kmin
   for (p.nimg = 2; p.nimg >= 1; --p.nimg)
     for (p.nstream = 2; p.nstream >= 1; --p.nstream)
       for (p.nband = 4; p.nband >= 2; --p.nband)
-        if (i8_layout(p).total <= budget) return true;
+        if (i8_layout(p).total <= budget) {
+          if (std::getenv("SIDWT_I8_VERBOSE")) {
+            const I8Smem L = i8_layout(p);
+            fprintf(stderr, "[i8] tn %d dmax %d rings: band %d x %d B, stream %d x %d B, img %d x %d B; staging at %zu, total %zu B\n",
+                    p.tn, p.dmax, p.nband, 2 * p.seg_alloc * 4, p.nstream, 2 * p.dmax * p.plane, p.nimg, p.img_alloc, L.stg, L.total);
+          }
+          return true;
+        }
   return false;
 }
 

@@ -24,7 +24,10 @@ using namespace sidwt;
 
 namespace {
 
-constexpr int kRV = 15;     // K1 run length (odd: bank-conflict free)
+#ifndef SIDWT_KRV
+#define SIDWT_KRV 15
+#endif
+constexpr int kRV = SIDWT_KRV;     // K1 run length (odd: bank-conflict free); 13 and 17 measured no better (A/B, -DSIDWT_KRV)
 constexpr int kQ = 9;       // K2 outputs per item (odd: bank-conflict free)
 constexpr int kK2NT = 256;  // K2 threads (Q = 11 with 192 threads measured slower on C2 and C5)
 
