@@ -31,17 +31,17 @@
 //   c = a + b itself (D + Tn - 1 groups of [128 lanes][32] int32), TMEM double-buffered by tile.
 //
 // Eq. (4): one CTA owns a whole row (persistent over rows), terms coarsest
-// first; every epilogue thread owns the same 16 lags of each 2048-lag tile for all terms, so
-// the running corr_i = corr_{i+1} + D_i lives in its registers; each corr_i goes straight to
-// HBM (128 contiguous bytes per thread) and the row's peak per scale (a7) is reduced in the
-// epilogue -- no partials, no finalize kernel.
+// first; every epilogue thread owns the same 16 lags (one lag block of one 2048-lag tile) for all
+// terms, so the running corr_i = corr_{i+1} + D_i lives in its registers; each corr_i goes
+// straight to HBM (128 contiguous bytes per thread) and the row's peak per scale (a7) is reduced
+// in the epilogue -- no partials, no finalize kernel.
 //
 // Roles (512 threads, whole warpgroups so that setmaxnreg can move registers to the epilogue):
 // warp 0 bulk-copy loader (band segments of both components, B images); warps 1, 2 MMA issuers
 // (whole warp, one elected lane issues; one tile each); warp 3 idle; warps 4-7 builders (int32
-// band segment -> byte-digit planes, range flag); warps 8-15 epilogue, two per TMEM lane quarter
-// (warp % 4), each eight of the 16 shifts of a lag block; corr leaves through swizzled staging
-// and TMA stores.
+// band segment -> byte-digit planes, range flag); warps 8-15 epilogue, one per TMEM lane quarter
+// (warp % 4) and tile (the row's two tiles in parallel), a thread takes all 16 shifts of its lag
+// block; corr leaves through swizzled staging and one 4 KB TMA store per warp and term.
 #define SIDWT_NO_KERNELS
 #include "kernels.cuh"
 #include "corr_tc.cuh"
