@@ -27,7 +27,12 @@ namespace {
 #ifndef SIDWT_KRV
 #define SIDWT_KRV 15
 #endif
-constexpr int kRV = SIDWT_KRV;     // K1 run length (odd: bank-conflict free); 13 and 17 measured no better (A/B, -DSIDWT_KRV)
+constexpr int kRV = SIDWT_KRV;     // K1 run length (odd: bank-conflict free), fused kernel and default
+// run length of the analysis kernel: 13 for deep plans (J >= 5) of the four-step 9/7 program (C3
+// analyze 2.14 -> 2.05 ms; C4, J = 4, is faster at 15: 0.39 vs 0.42 ms), 15 otherwise (C5: 4.59 ms
+// at 15, 4.92 at 13, 5.53 at 17; A/B with -DSIDWT_KRV)
+constexpr int kRV97 = SIDWT_KRV == 15 ? 13 : kRV;
+inline int rv_for(int fam, int J) { return (fam == F97 && J >= 5) ? kRV97 : kRV; }
 constexpr int kQ = 9;       // K2 outputs per item (odd: bank-conflict free)
 constexpr int kK2NT = 256;  // K2 threads (Q = 11 with 192 threads measured slower on C2 and C5)
 
@@ -76,6 +81,7 @@ struct sidwt_plan_s {
   bool ctaps = false;            // SIMT correlation reads the taps from its kernel parameters
   bool real_taps = false;        // every template tap has a zero imaginary part
   int run_chunks = 1;            // sidwt_run default chunk count
+  int ana_rv = kRV;              // K1 run length chosen at configure
   double t97 = 1.25;             // 9/7 lifting parameter t (Table I)
   // fused analyze -> correlate -> peaks (single template)
   bool fused = false;
@@ -246,6 +252,8 @@ static void configure(sidwt_plan_s* p) {
   p->stride = rup(ML + p->N + MR, 32);
 
   // ---- K1 tiling
+  const int rv = rv_for(p->fam, J);
+  p->ana_rv = rv;
   const Reach rc = dual_reach(p->fam);
   const int maxL = std::max(rc.lowL, rc.hiL);
   const int64_t halo_l = rup((int64_t)maxL * ((1LL << J) - 1), 4);
@@ -260,7 +268,7 @@ static void configure(sidwt_plan_s* p) {
     threads = 0;
     for (int s = 1; s <= J; ++s) {
       const int64_t h = 1LL << (s - 1);
-      threads = std::max(threads, h * cdiv(cdiv(lbuf, h), kRV));
+      threads = std::max(threads, h * cdiv(cdiv(lbuf, h), rv));
     }
     if ((lbuf <= lbuf_target && threads <= 512) || tile_len <= 32) break;
   }
@@ -275,7 +283,7 @@ static void configure(sidwt_plan_s* p) {
       threads = 0;
       for (int s = 1; s <= J; ++s) {
         const int64_t h = 1LL << (s - 1);
-        threads = std::max(threads, h * cdiv(cdiv(lbuf, h), kRV));
+        threads = std::max(threads, h * cdiv(cdiv(lbuf, h), rv));
       }
     }
   }
@@ -289,7 +297,7 @@ static void configure(sidwt_plan_s* p) {
   else if (p->fam == FD4) { HL = Dual<FD4>::HL; HR = Dual<FD4>::HR; }
   const int64_t htop = 1LL << (J - 1);
   p->ana.padl = (int)rup(HL * htop, 4);
-  p->ana.padr = (int)rup((kRV - 1 + HR) * htop, 4);
+  p->ana.padr = (int)rup((rv - 1 + HR) * htop, 4);
   p->ana_threads_needed = rup(threads, 32);
   p->ana_threads = (int)std::min<int64_t>(512, p->ana_threads_needed);
   p->ana_smem = (size_t)(p->ana.padl + 2 * (lbuf + p->ana.padr)) * 4;
@@ -636,7 +644,7 @@ int64_t sidwt_template_taps(sidwt_plan p, void* host_taps, int32_t* kmin, int32_
 // ---------------------------------------------------------------------------
 template <int FAM>
 static cudaError_t launch_analyze(const sidwt_plan_s* p, const void* rows, int64_t nrows, void* bands, cudaStream_t s) {
-  auto kern = k_analyze<FAM, kRV>;
+  auto kern = (FAM == F97 && p->ana_rv == kRV97) ? k_analyze<FAM, kRV97> : k_analyze<FAM, kRV>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->ana_smem);
   if (e != cudaSuccess) return e;
   AnaParams a = p->ana;
